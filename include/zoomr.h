@@ -1,0 +1,182 @@
+/*
+ * zoomr.h -- C-ABI of the B200-native ZoomR select + sparse-decode hot path
+ * (arXiv 2604.10898, "ZoomR").  Implemented by libzoomr.so (hand-written
+ * sm_100a CUDA kernels in paper_2604_10898_b200/csrc/).
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation / Algorithm 1 line),
+ * "S:n" = SPEC.md line n.  The readings of the paper that the kernels follow
+ * are listed in DESIGN.md section 3 (Q1..Q25).
+ *
+ * The five entry points are the five steps of the path, in order:
+ *   zoomr_update_mean_keys    a1  mean summary keys             P:36-41, Alg.1 @P:408-409
+ *   zoomr_score               a2  alpha = q.kbar, per-head top-k,
+ *                                 votes + sum-alpha aggregation  P:43-63, Alg.1 @P:411-417
+ *   zoomr_select_topc         a3  global top-c consensus         P:64-67, Alg.1 @P:418-419
+ *   zoomr_build_index         a4  multi-granularity index I_f    P:69-72, Alg.1 @P:421-422
+ *   zoomr_sparse_decode_attn  a5  paged gather + GQA decode
+ *                                 attention over I_f
+ *
+ * Conventions shared by every call
+ *  - Ownership: every array argument is DEVICE memory allocated and owned by
+ *    the caller.  The library never allocates device memory, never frees or
+ *    retains a pointer past the call, and has no global mutable state.  Host
+ *    structs (zoomr_geom, zoomr_kv, zoomr_segments) are read during the call only.
+ *  - Streams: `stream` is a cudaStream_t (passed as void*); all work is
+ *    enqueued on it asynchronously; no call synchronizes the host.  Every call
+ *    is CUDA-graph capturable.  Concurrent calls on different streams are safe
+ *    when their output and workspace buffers are distinct.
+ *  - Tokens: 0-based absolute positions.  Summary index i: 0-based; a smaller
+ *    index is an older summary (the tie-break, readings Q3/Q20).
+ *  - GQA: query head h reads KV head h / (H_q / H_kv) (reading Q6).  In the
+ *    KV-head-sharded mode the geometry holds the rank's LOCAL heads.
+ *  - Errors: the int return value is ZOOMR_OK or a host-detectable error
+ *    (NULL pointer, bad size, unsupported head_dim, launch failure); nothing is
+ *    enqueued when it is not ZOOMR_OK.  Data-dependent errors are detected on
+ *    the device and recorded, first one wins (atomicCAS from 0), into the
+ *    optional `dev_status` int32 (device memory, caller zeroes it); after a
+ *    device-detected error that sequence's outputs are defined but unspecified.
+ */
+#ifndef ZOOMR_H
+#define ZOOMR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZOOMR_ABI_VERSION 1
+
+typedef enum {
+  ZOOMR_OK = 0,
+  ZOOMR_ERR_INVALID_ARG = 1,   /* NULL pointer, negative size, top_k < 1, c < 0, ...     */
+  ZOOMR_ERR_DIM_MISMATCH = 2,  /* H_q % H_kv != 0, G = H_q/H_kv not in {1, 2, 4, 8}       */
+  ZOOMR_ERR_EMPTY_SEGMENT = 3, /* device: s1 <= s0 (SPEC EmptySegment)             */
+  ZOOMR_ERR_SEGMENT_ORDER = 4, /* device: r0<=r1<=s0<s1<=next r0 violated        */
+  ZOOMR_ERR_INDEX_RANGE = 5,   /* device: s1 > T, N_t > max_summaries, page beyond table  */
+  ZOOMR_ERR_CAPACITY = 6,      /* device: |I_f| > index_capacity (count is clamped)        */
+  ZOOMR_ERR_UNSUPPORTED = 7,   /* head_dim not in {16, 32, 64, 128}, N_t > 4096, k > 32   */
+  ZOOMR_ERR_CUDA = 8,          /* a CUDA launch failed                                     */
+  ZOOMR_ERR_WORKSPACE = 9      /* workspace smaller than zoomr_attn_workspace_bytes()      */
+} zoomr_status;
+
+/* Fixed-point scale of the aggregated score A_i in `partial` (reading Q2 +
+ * DESIGN.md "deterministic aggregation"): A_i is stored as the int64
+ * sum over voters of round(alpha * 2^32).  Integer addition is associative, so
+ * the value does not depend on accumulation order, on the number of ranks in
+ * the head-sharded all-reduce, or on the run. */
+#define ZOOMR_A_FRAC_BITS 32
+
+/* Model geometry.  heads are rank-local in the KV-head-sharded mode. */
+typedef struct {
+  int32_t num_layers;   /* N_L                                    */
+  int32_t num_q_heads;  /* H_q                                            */
+  int32_t num_kv_heads; /* H_kv; G = H_q / H_kv in {1, 2, 4, 8}            */
+  int32_t head_dim;     /* d in {16, 32, 64, 128}                         */
+  int32_t page_size;    /* P >= 1 tokens per KV page                      */
+} zoomr_geom;
+
+/* Paged KV cache (the paper's full cache K_t, V_t, held in HBM).
+ * k, v: bf16 [L][num_pages][H_kv][P][d] (element (l, p, g, j, e) at
+ *       (((l*num_pages + p)*H_kv + g)*P + j)*d + e).  16-byte aligned.
+ * page_table: int32 [B][max_pages]; token t of sequence b lives at physical
+ *       page page_table[b*max_pages + t/P], slot t%P.  Pages may alias across
+ *       sequences (read-only). */
+typedef struct {
+  const void *k;
+  const void *v;
+  int64_t num_pages;
+  const int32_t *page_table;
+  int32_t max_pages;
+} zoomr_kv;
+
+/* Segment table (the paper's R_i / S_i; SPEC SegmentMap S:22-28).
+ * bounds: int32 [B][max_summaries][4] = (r0, r1, s0, s1), half-open absolute
+ *         token ranges of R_i and S_i; only the first num_summaries[b] rows
+ *         (the CLOSED summaries, N_t) are read.  Must satisfy
+ *         r0 <= r1 <= s0 < s1 <= r0_{i+1} and s1 <= T (checked on device).
+ * num_summaries: int32 [B] = N_t.   seq_len: int32 [B] = T, tokens in the
+ *         cache counting the current one (T >= 1). */
+typedef struct {
+  const int32_t *bounds;
+  const int32_t *num_summaries;
+  const int32_t *seq_len;
+  int32_t max_summaries;
+} zoomr_segments;
+
+/* a1 -- mean summary keys, P:36-41 (eq. kbar_i = (1/|S_i|) sum_{j in S_i} k_j),
+ * Alg.1 @P:408-409.  For each item (b, i) in `items` (device int32 [n_items][2]),
+ * for every layer and KV head, writes
+ *   mean_keys[((b*L + l)*H_kv + g)*max_summaries + i][0..d)   (fp32)
+ * accumulated in fp64 from the bf16 keys of S_i = [s0_i, s1_i).  Entries not
+ * listed are untouched (the cache is written once per closed summary).
+ * Device errors: EMPTY_SEGMENT, INDEX_RANGE (i >= max_summaries or s1 > T or a
+ * page index beyond the page table). */
+int zoomr_update_mean_keys(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv,
+                           const zoomr_segments *seg, const int32_t *items, int32_t n_items,
+                           float *mean_keys, int32_t *dev_status, void *stream);
+
+/* a2 -- scoring, per-head voting and aggregation, Alg.1 @P:411-417.
+ *   alpha[b,l,h,i] = q[b,l,h] . kbar[b,l,h/G,i]         (fp32, no 1/sqrt(d): P:45, reading Q7)
+ *   per voter (l,h): top-min(k, N_t) summaries by (alpha desc, i asc)  (reading Q3/Q5)
+ *   partial[b][0][i] = v_i = number of voters that chose i
+ *   partial[b][1][i] = A_i = sum over those voters of round(alpha*2^32) (reading Q2)
+ * q: bf16 [B][L][H_q][d].  mean_keys: fp32 as written by a1.  partial: int64
+ * [B][2][max_summaries], fully overwritten (entries i >= N_t are 0).  In the
+ * KV-head-sharded mode each rank passes its local heads and the caller sums
+ * `partial` across ranks (one all-reduce) before a3.
+ * alpha_out (nullable): fp32 [B][L][H_q][max_summaries].  topk_out (nullable):
+ * int32 [B][L*H_q][top_k], -1 past min(k, N_t).  1 <= top_k <= 32.
+ * Device errors: INDEX_RANGE (N_t > max_summaries), UNSUPPORTED (N_t > 4096). */
+int zoomr_score(const zoomr_geom *geom, int32_t batch, const void *q, const float *mean_keys,
+                const int32_t *num_summaries, int32_t max_summaries, int32_t top_k,
+                int64_t *partial, float *alpha_out, int32_t *topk_out, int32_t *dev_status,
+                void *stream);
+
+/* a3 -- global consensus top-c, Alg.1 @P:418-419.
+ * I_all = {i < N_t : v_i > 0}; I_c = the first min(c, |I_all|) of I_all in the
+ * order (v desc, A desc, i asc) (readings Q2/Q5); I_s = I_all \ I_c.
+ * flags: uint8 [B][max_summaries], 2 for I_c (zoom into R_i), 1 for I_s (keep
+ * S_i), 0 otherwise (entries i >= N_t are 0).  agreeability (nullable): fp32
+ * [B], AG = sum_{I_c} v / sum_{I_all} v (0 when I_all is empty). */
+int zoomr_select_topc(int32_t batch, const int64_t *partial, const int32_t *num_summaries,
+                      int32_t max_summaries, int32_t c, uint8_t *flags, float *agreeability,
+                      int32_t *dev_status, void *stream);
+
+/* a4 -- the multi-granularity index set, P:69-72 (eq. I_f = I_p u I_w u R(I_c) u S(I_s)),
+ * Alg.1 @P:421-422.  I_p = [0, min(sink, T)) (reading Q12), I_w = [max(0, T-window), T)
+ * (reading Q13: the window holds the current token), R_i for flag 2, S_i for flag 1.
+ * Writes the sorted set union to index[b*index_capacity + 0 .. count) and
+ * index_count[b] = |I_f|.  If |I_f| > index_capacity the list is truncated to
+ * the capacity and CAPACITY is recorded.  window >= 1, sink >= 0.  flags may be
+ * NULL when every N_t is 0. */
+int zoomr_build_index(int32_t batch, const zoomr_segments *seg, const uint8_t *flags,
+                      int32_t sink, int32_t window, int32_t *index, int32_t index_capacity,
+                      int32_t *index_count, int32_t *dev_status, void *stream);
+
+/* Workspace for a5: split-K partial results and per-(b,l,g) arrival counters.
+ * Must be zero-filled once before the first call; every call leaves it zeroed. */
+size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
+
+/* a5 -- sparse GQA decode attention over I_f, P:74 and P:145-149:
+ *   out[b,l,h] = sum_{j in I_f,b} softmax_j(q[b,l,h] . k_j * softmax_scale) v_j
+ * with k_j, v_j of KV head h/G gathered from the paged pool.  fp32 logits,
+ * online softmax and accumulation; out fp32 [B][L][H_q][d].  index / index_count
+ * as written by a4 (count >= 1).  softmax_scale is normally 1/sqrt(d). */
+int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
+                             const zoomr_kv *kv, const int32_t *index,
+                             const int32_t *index_count, int32_t index_capacity,
+                             float softmax_scale, float *out, void *workspace,
+                             size_t workspace_bytes, int32_t *dev_status, void *stream);
+
+/* Human-readable status name; never NULL. */
+const char *zoomr_status_str(int status);
+
+/* ZOOMR_ABI_VERSION of the loaded library. */
+int zoomr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZOOMR_H */

@@ -1,0 +1,61 @@
+// common.cuh -- shared device/host helpers of libzoomr (sm_100a).
+// Product code: never includes or links anything under oracle/.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/zoomr.h"
+
+namespace zoomr {
+
+constexpr int kMaxSummaries = 4096;  // N_max supported by a2/a3/a4 (shared-memory resident)
+constexpr int kMaxTopK = 32;
+
+// First device-detected error wins (zoomr.h "Errors").
+__device__ __forceinline__ void set_status(int32_t *st, int32_t code) {
+  if (st) atomicCAS(st, 0, code);
+}
+
+__device__ __forceinline__ float bf16lo_to_float(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi_to_float(uint32_t w) {
+  return __uint_as_float(w & 0xffff0000u);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ZOOMR_OK : ZOOMR_ERR_CUDA;
+}
+
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  }
+  return n;
+}
+
+inline bool valid_geom(const zoomr_geom *g) {
+  if (!g) return false;
+  if (g->num_layers < 1 || g->num_q_heads < 1 || g->num_kv_heads < 1 || g->page_size < 1) return false;
+  return true;
+}
+
+inline int check_geom(const zoomr_geom *g) {
+  if (!valid_geom(g)) return ZOOMR_ERR_INVALID_ARG;
+  if (g->num_q_heads % g->num_kv_heads) return ZOOMR_ERR_DIM_MISMATCH;
+  int G = g->num_q_heads / g->num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return ZOOMR_ERR_DIM_MISMATCH;
+  int d = g->head_dim;
+  if (d != 16 && d != 32 && d != 64 && d != 128) return ZOOMR_ERR_UNSUPPORTED;
+  return ZOOMR_OK;
+}
+
+}  // namespace zoomr

@@ -1,0 +1,630 @@
+// a5 -- sparse GQA decode attention over the selected index set
+// ("the attention mechanism will compute over the keys and values
+// corresponding only to the indices in I_f"; attention equation):
+//
+//   o^{(l,h)} = sum_{j in I_f} softmax_j( q^{(l,h)} . k_j^{(l,h/G)} * scale ) v_j^{(l,h/G)}
+//
+// B200 design:
+//  * Work = the flattened sequence of 32-token tiles of every (b, l, g)
+//    segment.  A persistent grid (one CTA per SM) gives each consumer warp a
+//    contiguous, equal share of that sequence ("stream-K" split): perfect load
+//    balance whatever |I_f| turns out to be on the device, and at most two
+//    partial results per warp.  Segments split across warps are merged by the
+//    last-arriving warp (arrival counter per segment, self-resetting).
+//  * Gather: one producer warp per CTA turns I_f positions into paged row
+//    addresses (page table lookup) and issues one TMA bulk copy
+//    (cp.async.bulk, UBLKCP) per K row and per V row straight into a
+//    multi-stage shared-memory ring, completing on an mbarrier (expect_tx).
+//    Rows land at a 2*d+16 byte stride so the ldmatrix reads below are
+//    bank-conflict free.
+//  * Math on tensor cores (mma.sync m16n8k16, bf16 in, fp32 accumulate):
+//      S^T-tile = K_tile (32 tok x d) . Q^T (d x 8 padded heads)
+//      O^T     += V_tile^T (d x 32 tok) . P (32 tok x 8)
+//    The G query heads of the KV head share every gathered K/V tile (GQA).
+//    The 8 MMA columns hold the G heads twice: P is split p = hi + lo into two
+//    bf16 values (hi = bf16(p), lo = bf16(p - hi)) in the two copies, so the PV
+//    product carries ~16 bits of P (bf16 alone would cost up to ~8e-3 abs,
+//    SURVEY 7.3-1) at no extra MMA for G <= 4.  The S accumulator fragment is
+//    transposed into the PV B-operand with movmatrix.
+//  * fp32 online softmax (exp2 with scale*log2e folded in), fp32 output.
+#include "common.cuh"
+
+namespace zoomr {
+
+constexpr int kTile = 32;  // tokens per consumer tile (one per producer lane)
+constexpr int kNCW = 4;    // consumer warps per CTA
+constexpr int kNSW = 3;    // ring stages per consumer warp
+
+template <int D>
+struct AttnShape {
+  static constexpr int RB = 2 * D;              // bytes of one K or V row (bf16)
+  static constexpr int RS = 2 * D + 16;         // padded smem row stride (conflict-free ldmatrix)
+  static constexpr int TILE_BYTES = kTile * RS;  // K (or V) part of a stage
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+  static constexpr int RING_BYTES = kNCW * kNSW * STAGE_BYTES;
+};
+
+struct AttnParams {
+  const __nv_bfloat16 *q;
+  const __nv_bfloat16 *kpool;
+  const __nv_bfloat16 *vpool;
+  int64_t num_pages;
+  const int32_t *page_table;
+  int32_t max_pages;
+  const int32_t *index;
+  const int32_t *count;
+  int32_t cap;
+  float *out;
+  float *ws_part;      // [NW][2][G*(D+2)]
+  int32_t *ws_cnt;     // [B*L*Hkv]
+  int32_t B, L, Hkv, P;
+  float scale_log2;
+  int32_t *status;
+};
+
+// ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// ----------------------------------------------------------- tile geometry --
+struct Sched {
+  const int32_t *prefix;  // smem [B+1]: first global tile of sequence b
+  int64_t T_tot;
+  int64_t NWe;            // effective number of warps (<= T_tot)
+  int32_t B, LH;          // LH = L * Hkv segments per sequence
+  __device__ __forceinline__ int64_t range_start(int64_t w) const { return T_tot * w / NWe; }
+  __device__ __forceinline__ int64_t warp_of(int64_t t) const { return ((t + 1) * NWe - 1) / T_tot; }
+  // global tile -> (b, segment within b, tile within segment, tiles per segment of b)
+  __device__ __forceinline__ void locate(int64_t t, int &b, int &seg, int &tis, int &nts) const {
+    int lo = 0, hi = B - 1;
+    while (lo < hi) {  // last b with prefix[b] <= t
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    b = lo;
+    nts = (prefix[b + 1] - prefix[b]) / LH;
+    const int r = (int)(t - prefix[b]);
+    seg = r / nts;
+    tis = r - seg * nts;
+  }
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const AttnParams p) {
+  using S = AttnShape<D>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kNCW][kNSW]
+  uint64_t *empty = full + kNCW * kNSW;                                 // [kNCW][kNSW]
+  int32_t *prefix = reinterpret_cast<int32_t *>(empty + kNCW * kNSW);   // [B+1]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Hq = p.Hkv * G;
+
+  if (threadIdx.x == 0) {
+    for (int x = 0; x < kNCW * kNSW; ++x) {
+      mbar_init(&full[x], 1);
+      mbar_init(&empty[x], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // tiles per sequence -> prefix (B is small; warp 0 scans in chunks of 32)
+  if (warp == 0) {
+    int carry = 0;
+    for (int b0 = 0; b0 < p.B; b0 += 32) {
+      const int b = b0 + lane;
+      int n = 0;
+      if (b < p.B) {
+        int c = p.count[b];
+        c = c < p.cap ? c : p.cap;
+        n = c > 0 ? (c + kTile - 1) / kTile * p.L * p.Hkv : 0;
+      }
+      int incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (b < p.B) prefix[b] = carry + incl - n;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) prefix[p.B] = carry;
+  }
+  __syncthreads();
+
+  Sched sc;
+  sc.prefix = prefix;
+  sc.T_tot = prefix[p.B];
+  sc.B = p.B;
+  sc.LH = p.L * p.Hkv;
+  if (sc.T_tot == 0) return;
+  const int64_t NW = (int64_t)gridDim.x * kNCW;
+  sc.NWe = NW < sc.T_tot ? NW : sc.T_tot;
+
+  if (warp == kNCW) {
+    // ======================= producer: paged gather via TMA bulk copies =====
+    int64_t r0[kNCW], nt[kNCW];
+#pragma unroll
+    for (int w = 0; w < kNCW; ++w) {
+      const int64_t gw = (int64_t)blockIdx.x * kNCW + w;
+      if (gw < sc.NWe) {
+        r0[w] = sc.range_start(gw);
+        nt[w] = sc.range_start(gw + 1) - r0[w];
+      } else {
+        r0[w] = 0;
+        nt[w] = 0;
+      }
+    }
+    int64_t kmax = 0;
+#pragma unroll
+    for (int w = 0; w < kNCW; ++w) kmax = nt[w] > kmax ? nt[w] : kmax;
+    const uint32_t ring = smem_u32(smem);
+    for (int64_t k = 0; k < kmax; ++k) {
+      // phase 1: resolve this round's rows for every consumer warp (independent loads in flight)
+      const __nv_bfloat16 *ksrc[kNCW], *vsrc[kNCW];
+      int nvalid[kNCW];
+#pragma unroll
+      for (int w = 0; w < kNCW; ++w) {
+        ksrc[w] = nullptr;
+        vsrc[w] = nullptr;
+        nvalid[w] = 0;
+        if (k < nt[w]) {
+          int b, seg, tis, nts;
+          sc.locate(r0[w] + k, b, seg, tis, nts);
+          int cnt = p.count[b];
+          cnt = cnt < p.cap ? cnt : p.cap;
+          const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+          const int pos0 = tis * kTile;
+          nvalid[w] = min(kTile, cnt - pos0);
+          if (lane < nvalid[w]) {
+            const int tok = p.index[(int64_t)b * p.cap + pos0 + lane];
+            const int lp = tok / p.P;
+            int page = 0;
+            if (tok >= 0 && lp < p.max_pages) page = p.page_table[(int64_t)b * p.max_pages + lp];
+            if (tok < 0 || lp >= p.max_pages || page < 0 || page >= p.num_pages) {
+              set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+              page = 0;
+            }
+            const int64_t row = (((int64_t)l * p.num_pages + page) * p.Hkv + g) * p.P + (tok - lp * p.P);
+            ksrc[w] = p.kpool + row * D;
+            vsrc[w] = p.vpool + row * D;
+          }
+        }
+      }
+      // phase 2: claim the stage and launch the copies
+#pragma unroll
+      for (int w = 0; w < kNCW; ++w) {
+        if (k >= nt[w]) continue;
+        const int s = (int)(k % kNSW);
+        const uint32_t par = (uint32_t)((k / kNSW) & 1);
+        mbar_wait(&empty[w * kNSW + s], par ^ 1u);
+        const uint32_t stK = ring + (uint32_t)((w * kNSW + s) * S::STAGE_BYTES);
+        const uint32_t stV = stK + S::TILE_BYTES;
+        if (lane >= nvalid[w]) {
+          // rows past the end of the segment: zero V so that P = 0 cannot meet stale NaNs
+          uint4 *vr = reinterpret_cast<uint4 *>(smem + (stV - ring) + lane * S::RS);
+#pragma unroll
+          for (int x = 0; x < S::RB / 16; ++x) vr[x] = make_uint4(0, 0, 0, 0);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[w * kNSW + s], (uint32_t)(nvalid[w] * 2 * S::RB));
+        __syncwarp();
+        if (lane < nvalid[w]) {
+          bulk_g2s(stK + lane * S::RS, ksrc[w], S::RB, &full[w * kNSW + s]);
+          bulk_g2s(stV + lane * S::RS, vsrc[w], S::RB, &full[w * kNSW + s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ========================= consumers: tensor-core flash-decode ============
+  const int64_t gw = (int64_t)blockIdx.x * kNCW + warp;
+  if (gw >= sc.NWe) return;
+  const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
+  const int gq = lane >> 2, tq = lane & 3;  // mma fragment row group / thread-in-group
+  const int n0 = 2 * tq;                    // the two MMA columns this thread holds: n0, n0+1
+  constexpr int NKS = D / 16;               // k-steps of QK^T and m-tiles of O^T
+  constexpr bool kTwoN = (G == 8);          // hi and lo in separate n-tiles
+  // column -> (head, part) for G <= 4: head = n % G, part = n / G (0 hi, 1 lo, >=2 none)
+  const int part0 = kTwoN ? 0 : n0 / G, part1 = kTwoN ? 0 : (n0 + 1) / G;
+
+  int first_b = -1, first_seg = -1;  // the first segment of this warp's range (slot rule)
+  int cur_b = -1, cur_seg = -1;
+  uint32_t qf[NKS][2];
+  float o[NKS][4], o2[kTwoN ? NKS : 1][4];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const uint32_t ring = smem_u32(smem);
+
+  auto flush = [&](int b, int seg) {
+    // finish the segment's softmax state and publish it (final or partial)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    float ov[NKS][4];
+#pragma unroll
+    for (int me = 0; me < NKS; ++me)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        float v = o[me][x];
+        if constexpr (G == 8) v += o2[me][x];
+        else if constexpr (G == 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
+        else if constexpr (G == 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
+        ov[me][x] = v;
+      }
+    if constexpr (G == 1) {
+#pragma unroll
+      for (int me = 0; me < NKS; ++me) {
+        ov[me][0] += ov[me][1];
+        ov[me][2] += ov[me][3];
+      }
+    }
+    // owners: threads whose columns are the hi copies of real heads
+    const bool owner = (G == 8) || (G == 4 && tq < 2) || (G <= 2 && tq == 0);
+    const int nh = (G == 1) ? 1 : 2;  // heads held by an owner thread: n0 (and n0+1)
+    const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+    const int nts = (sc.prefix[b + 1] - sc.prefix[b]) / sc.LH;
+    const int64_t st0 = sc.prefix[b] + (int64_t)seg * nts, st1 = st0 + nts;
+    const int64_t wf = sc.warp_of(st0), wl = sc.warp_of(st1 - 1);
+    if (wf == wl) {  // this warp owns the whole segment: final output
+      if (owner) {
+        const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+        float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
+#pragma unroll
+        for (int me = 0; me < NKS; ++me) {
+          const int e = me * 16 + gq;
+          ob[(int64_t)n0 * D + e] = ov[me][0] * inv0;
+          ob[(int64_t)n0 * D + e + 8] = ov[me][2] * inv0;
+          if (nh == 2) {
+            ob[(int64_t)(n0 + 1) * D + e] = ov[me][1] * inv1;
+            ob[(int64_t)(n0 + 1) * D + e + 8] = ov[me][3] * inv1;
+          }
+        }
+      }
+      return;
+    }
+    // partial: slot 0 if this is the warp's first segment, else slot 1
+    constexpr int SLOT = G * (D + 2);
+    const int slot = (b == first_b && seg == first_seg) ? 0 : 1;
+    float *ps = p.ws_part + ((int64_t)gw * 2 + slot) * SLOT;
+    if (owner) {
+      if (gq == 0) {
+        ps[n0] = m0;
+        ps[G + n0] = l0;
+        if (nh == 2) {
+          ps[n0 + 1] = m1;
+          ps[G + n0 + 1] = l1;
+        }
+      }
+#pragma unroll
+      for (int me = 0; me < NKS; ++me) {
+        const int e = me * 16 + gq;
+        ps[2 * G + n0 * D + e] = ov[me][0];
+        ps[2 * G + n0 * D + e + 8] = ov[me][2];
+        if (nh == 2) {
+          ps[2 * G + (n0 + 1) * D + e] = ov[me][1];
+          ps[2 * G + (n0 + 1) * D + e + 8] = ov[me][3];
+        }
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    int32_t *cnt = p.ws_cnt + (int64_t)b * sc.LH + seg;
+    int old = 0;
+    if (lane == 0) old = atomicAdd(cnt, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != (int)(wl - wf)) return;  // not the last arriving warp
+    __threadfence();
+    // last arriver: merge the partials of warps wf..wl in order
+    for (int x = lane; x < G * D; x += 32) {
+      const int h = x / D, e = x - h * D;
+      float M = -INFINITY;
+      for (int64_t w2 = wf; w2 <= wl; ++w2) {
+        int fb, fs, ft, fn;
+        sc.locate(sc.range_start(w2), fb, fs, ft, fn);
+        const int sl = (fb == b && fs == seg) ? 0 : 1;
+        const float *q2 = p.ws_part + (w2 * 2 + sl) * SLOT;
+        M = fmaxf(M, __ldcg(q2 + h));
+      }
+      float Lsum = 0.f, Osum = 0.f;
+      for (int64_t w2 = wf; w2 <= wl; ++w2) {
+        int fb, fs, ft, fn;
+        sc.locate(sc.range_start(w2), fb, fs, ft, fn);
+        const int sl = (fb == b && fs == seg) ? 0 : 1;
+        const float *q2 = p.ws_part + (w2 * 2 + sl) * SLOT;
+        const float sc2 = ex2(__ldcg(q2 + h) - M);
+        Lsum += __ldcg(q2 + G + h) * sc2;
+        Osum += __ldcg(q2 + 2 * G + h * D + e) * sc2;
+      }
+      p.out[(((int64_t)b * p.L + l) * Hq + (int64_t)g * G + h) * D + e] = Osum / Lsum;
+    }
+    if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
+  };
+
+  for (int64_t k = 0; r0 + k < r1; ++k) {
+    int b, seg, tis, nts;
+    sc.locate(r0 + k, b, seg, tis, nts);
+    if (k == 0) {
+      first_b = b;
+      first_seg = seg;
+    }
+    if (b != cur_b || seg != cur_seg) {
+      if (cur_b >= 0) flush(cur_b, cur_seg);
+      cur_b = b;
+      cur_seg = seg;
+      // Q fragments (B operand of QK^T): Q[head n % G][k-chunk], this thread's column n = gq
+      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      const __nv_bfloat16 *qh = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G + (gq % G)) * D;
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        qf[ks][0] = *reinterpret_cast<const uint32_t *>(qh + ks * 16 + 2 * tq);
+        qf[ks][1] = *reinterpret_cast<const uint32_t *>(qh + ks * 16 + 8 + 2 * tq);
+      }
+#pragma unroll
+      for (int me = 0; me < NKS; ++me)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          o[me][x] = 0.f;
+          if constexpr (kTwoN) o2[me][x] = 0.f;
+        }
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+    }
+    int cnt = p.count[b];
+    cnt = cnt < p.cap ? cnt : p.cap;
+    const int nvalid = min(kTile, cnt - tis * kTile);
+    const int s = (int)(k % kNSW);
+    mbar_wait(&full[warp * kNSW + s], (uint32_t)((k / kNSW) & 1));
+    const uint32_t stK = ring + (uint32_t)((warp * kNSW + s) * S::STAGE_BYTES);
+    const uint32_t stV = stK + S::TILE_BYTES;
+
+    // ---- S = K . Q^T  (2 m-tiles of 16 tokens) ----
+    float sacc[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) sacc[mt][x] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < NKS; ++ks) {
+        uint32_t a0, a1, a2, a3;
+        const int row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x4(stK + row * S::RS + (ks * 2 + (lane >> 4)) * 16, a0, a1, a2, a3);
+        mma_bf16(sacc[mt], a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
+      }
+    }
+    // ---- online softmax over the tile's tokens, per column ----
+    float cm0 = -INFINITY, cm1 = -INFINITY;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int t0 = mt * 16 + gq, t1 = t0 + 8;
+      sacc[mt][0] = t0 < nvalid ? sacc[mt][0] * p.scale_log2 : -INFINITY;
+      sacc[mt][1] = t0 < nvalid ? sacc[mt][1] * p.scale_log2 : -INFINITY;
+      sacc[mt][2] = t1 < nvalid ? sacc[mt][2] * p.scale_log2 : -INFINITY;
+      sacc[mt][3] = t1 < nvalid ? sacc[mt][3] * p.scale_log2 : -INFINITY;
+      cm0 = fmaxf(cm0, fmaxf(sacc[mt][0], sacc[mt][2]));
+      cm1 = fmaxf(cm1, fmaxf(sacc[mt][1], sacc[mt][3]));
+    }
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, off));
+      cm1 = fmaxf(cm1, __shfl_xor_sync(0xffffffffu, cm1, off));
+    }
+    const float mn0 = fmaxf(m0, cm0), mn1 = fmaxf(m1, cm1);
+    const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // m = -inf -> 0
+    m0 = mn0;
+    m1 = mn1;
+    float ps0 = 0.f, ps1 = 0.f;
+    uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const float p00 = ex2(sacc[mt][0] - mn0), p01 = ex2(sacc[mt][1] - mn1);
+      const float p10 = ex2(sacc[mt][2] - mn0), p11 = ex2(sacc[mt][3] - mn1);
+      ps0 += p00 + p10;
+      ps1 += p01 + p11;
+      // hi = bf16(p), lo = bf16(p - hi)
+      const float h00 = __bfloat162float(__float2bfloat16_rn(p00));
+      const float h01 = __bfloat162float(__float2bfloat16_rn(p01));
+      const float h10 = __bfloat162float(__float2bfloat16_rn(p10));
+      const float h11 = __bfloat162float(__float2bfloat16_rn(p11));
+      if constexpr (kTwoN) {
+        bh[mt][0] = movm_t(pack_bf16(h00, h01));
+        bh[mt][1] = movm_t(pack_bf16(h10, h11));
+        bl[mt][0] = movm_t(pack_bf16(p00 - h00, p01 - h01));
+        bl[mt][1] = movm_t(pack_bf16(p10 - h10, p11 - h11));
+      } else {
+        const float v00 = part0 == 0 ? h00 : (part0 == 1 ? p00 - h00 : 0.f);
+        const float v01 = part1 == 0 ? h01 : (part1 == 1 ? p01 - h01 : 0.f);
+        const float v10 = part0 == 0 ? h10 : (part0 == 1 ? p10 - h10 : 0.f);
+        const float v11 = part1 == 0 ? h11 : (part1 == 1 ? p11 - h11 : 0.f);
+        bh[mt][0] = movm_t(pack_bf16(v00, v01));
+        bh[mt][1] = movm_t(pack_bf16(v10, v11));
+      }
+    }
+    l0 = l0 * al0 + ps0;
+    l1 = l1 * al1 + ps1;
+    // ---- O^T = alpha * O^T + V^T . P ----
+#pragma unroll
+    for (int me = 0; me < NKS; ++me) {
+      o[me][0] *= al0;
+      o[me][1] *= al1;
+      o[me][2] *= al0;
+      o[me][3] *= al1;
+      if constexpr (kTwoN) {
+        o2[me][0] *= al0;
+        o2[me][1] *= al1;
+        o2[me][2] *= al0;
+        o2[me][3] *= al1;
+      }
+#pragma unroll
+      for (int kt = 0; kt < 2; ++kt) {
+        uint32_t a0, a1, a2, a3;
+        const int row = kt * 16 + (lane & 7) + ((lane >> 4) & 1) * 8;
+        ldsm_x4_t(stV + row * S::RS + (me * 2 + ((lane >> 3) & 1)) * 16, a0, a1, a2, a3);
+        mma_bf16(o[me], a0, a1, a2, a3, bh[kt][0], bh[kt][1]);
+        if constexpr (kTwoN) mma_bf16(o2[me], a0, a1, a2, a3, bl[kt][0], bl[kt][1]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[warp * kNSW + s]);
+  }
+  if (cur_b >= 0) flush(cur_b, cur_seg);
+}
+
+template <int D, int G>
+size_t attn_smem_bytes(int B) {
+  return (size_t)AttnShape<D>::RING_BYTES + 2 * kNCW * kNSW * sizeof(uint64_t) + (size_t)(B + 1) * sizeof(int32_t);
+}
+
+inline int attn_grid() { return num_sms(); }
+
+inline size_t attn_ws_part_floats(const zoomr_geom *g) {
+  const int G = g->num_q_heads / g->num_kv_heads;
+  return (size_t)attn_grid() * kNCW * 2 * G * (g->head_dim + 2);
+}
+
+}  // namespace zoomr
+
+using namespace zoomr;
+
+extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch) {
+  if (check_geom(geom) || batch < 1) return 0;
+  const size_t part = attn_ws_part_floats(geom) * sizeof(float);
+  const size_t cnt = (size_t)batch * geom->num_layers * geom->num_kv_heads * sizeof(int32_t);
+  return ((part + 255) / 256) * 256 + cnt;
+}
+
+extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
+                                        const zoomr_kv *kv, const int32_t *index,
+                                        const int32_t *index_count, int32_t index_capacity,
+                                        float softmax_scale, float *out, void *workspace,
+                                        size_t workspace_bytes, int32_t *dev_status, void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !q || !kv || !kv->k || !kv->v || !kv->page_table || !index || !index_count ||
+      index_capacity < 1 || !out || !workspace || kv->num_pages < 1 || kv->max_pages < 1)
+    return ZOOMR_ERR_INVALID_ARG;
+  if (batch > 65536) return ZOOMR_ERR_UNSUPPORTED;
+  const size_t need = zoomr_attn_workspace_bytes(geom, batch);
+  if (workspace_bytes < need) return ZOOMR_ERR_WORKSPACE;
+  AttnParams prm;
+  prm.q = (const __nv_bfloat16 *)q;
+  prm.kpool = (const __nv_bfloat16 *)kv->k;
+  prm.vpool = (const __nv_bfloat16 *)kv->v;
+  prm.num_pages = kv->num_pages;
+  prm.page_table = kv->page_table;
+  prm.max_pages = kv->max_pages;
+  prm.index = index;
+  prm.count = index_count;
+  prm.cap = index_capacity;
+  prm.out = out;
+  const size_t part = attn_ws_part_floats(geom) * sizeof(float);
+  prm.ws_part = (float *)workspace;
+  prm.ws_cnt = (int32_t *)((char *)workspace + ((part + 255) / 256) * 256);
+  prm.B = batch;
+  prm.L = geom->num_layers;
+  prm.Hkv = geom->num_kv_heads;
+  prm.P = geom->page_size;
+  prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+  prm.status = dev_status;
+  const int G = geom->num_q_heads / geom->num_kv_heads;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = attn_grid();
+#define ZOOMR_AT(DD, GG)                                                                             \
+  do {                                                                                               \
+    auto kfn = sparse_attn_kernel<DD, GG>;                                                           \
+    const size_t smem = attn_smem_bytes<DD, GG>(batch);                                              \
+    if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                             \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);               \
+    kfn<<<grid, 32 * (kNCW + 1), smem, s>>>(prm);                                                    \
+  } while (0)
+#define ZOOMR_AT_G(DD)                 \
+  switch (G) {                         \
+    case 1: ZOOMR_AT(DD, 1); break;    \
+    case 2: ZOOMR_AT(DD, 2); break;    \
+    case 4: ZOOMR_AT(DD, 4); break;    \
+    default: ZOOMR_AT(DD, 8); break;   \
+  }
+  switch (geom->head_dim) {
+    case 16: ZOOMR_AT_G(16); break;
+    case 32: ZOOMR_AT_G(32); break;
+    case 64: ZOOMR_AT_G(64); break;
+    default: ZOOMR_AT_G(128); break;
+  }
+#undef ZOOMR_AT_G
+#undef ZOOMR_AT
+  return launch_status();
+}
+
+extern "C" const char *zoomr_status_str(int status) {
+  switch (status) {
+    case ZOOMR_OK: return "ZOOMR_OK";
+    case ZOOMR_ERR_INVALID_ARG: return "ZOOMR_ERR_INVALID_ARG";
+    case ZOOMR_ERR_DIM_MISMATCH: return "ZOOMR_ERR_DIM_MISMATCH";
+    case ZOOMR_ERR_EMPTY_SEGMENT: return "ZOOMR_ERR_EMPTY_SEGMENT";
+    case ZOOMR_ERR_SEGMENT_ORDER: return "ZOOMR_ERR_SEGMENT_ORDER";
+    case ZOOMR_ERR_INDEX_RANGE: return "ZOOMR_ERR_INDEX_RANGE";
+    case ZOOMR_ERR_CAPACITY: return "ZOOMR_ERR_CAPACITY";
+    case ZOOMR_ERR_UNSUPPORTED: return "ZOOMR_ERR_UNSUPPORTED";
+    case ZOOMR_ERR_CUDA: return "ZOOMR_ERR_CUDA";
+    case ZOOMR_ERR_WORKSPACE: return "ZOOMR_ERR_WORKSPACE";
+    default: return "ZOOMR_ERR_UNKNOWN";
+  }
+}
+
+extern "C" int zoomr_abi_version(void) { return ZOOMR_ABI_VERSION; }

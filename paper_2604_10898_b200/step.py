@@ -1,0 +1,114 @@
+"""One ZoomR decode step on the device: a1 -> a2 -> [all-reduce] -> a3 -> a4 -> a5.
+
+Owns the step's device buffers (mean-key cache, partial votes, flags, index
+set, output, attention workspace) and enqueues the five libzoomr kernels in
+Algorithm 1's order.  Optionally captures the whole step in a CUDA
+graph so a decode step is one graph launch.  Marshalling and scheduling only:
+every arithmetic step runs in the CUDA kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+
+from . import zoomr as Z
+
+
+@dataclass
+class StepParams:
+    top_k: int
+    c: int
+    sink: int
+    window: int
+
+
+class ZoomrStep:
+    """Device state + launch sequence of one (rank-local) decode step."""
+
+    def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
+                 params: StepParams, device="cuda", debug_outputs: bool = False):
+        self.shape, self.batch, self.params = shape, batch, params
+        self.max_summaries, self.cap = max_summaries, index_capacity
+        dev = torch.device(device)
+        L, Hq, Hkv, d = shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
+        self.mean_keys = torch.zeros(batch, L, Hkv, max_summaries, d, dtype=torch.float32, device=dev)
+        self.partial = torch.zeros(batch, 2, max_summaries, dtype=torch.int64, device=dev)
+        self.flags = torch.zeros(batch, max_summaries, dtype=torch.uint8, device=dev)
+        self.index = torch.zeros(batch, index_capacity, dtype=torch.int32, device=dev)
+        self.count = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.out = torch.zeros(batch, L, Hq, d, dtype=torch.float32, device=dev)
+        self.agreeability = torch.zeros(batch, dtype=torch.float32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = Z.attn_workspace_bytes(shape, batch)
+        self.workspace = torch.zeros(max(ws, 1), dtype=torch.uint8, device=dev)
+        self.alpha = self.topk = None
+        if debug_outputs:
+            self.alpha = torch.zeros(batch, L, Hq, max_summaries, dtype=torch.float32, device=dev)
+            self.topk = torch.zeros(batch, L * Hq, params.top_k, dtype=torch.int32, device=dev)
+        self.graph = None
+
+    # -- a1: mean keys for a list of closed summaries (b, i) --------------------
+    def update_mean_keys(self, kv, seg, items: torch.Tensor):
+        k_pool, v_pool, page_table = kv
+        bounds, nsum, seq_len = seg
+        Z.update_mean_keys(self.shape, k_pool, v_pool, page_table, bounds, nsum, seq_len, items,
+                           self.mean_keys, self.status)
+
+    @staticmethod
+    def all_items(num_summaries: torch.Tensor) -> torch.Tensor:
+        """(b, i) for every closed summary (host-side list for the initial cache build)."""
+        ns = num_summaries.cpu().tolist()
+        items = [(b, i) for b, n in enumerate(ns) for i in range(n)]
+        t = torch.tensor(items if items else [[0, 0]], dtype=torch.int32)
+        return t[: len(items)].to(num_summaries.device)
+
+    # -- the step ----------------------------------------------------------------
+    def run(self, q, kv, seg, update_selection: bool = True, close_items: Optional[torch.Tensor] = None,
+            allreduce: Optional[Callable[[torch.Tensor], None]] = None):
+        """Enqueue one decode step on the current stream.
+
+        close_items: summaries that closed since the last step (a1, amortized).
+        update_selection: run a2/a3 (a semantic-boundary / every-U step);
+            otherwise the held flags are reused and only a4/a5 run (reading Q14).
+        allreduce: the KV-head-sharded exchange of `partial` (sum over ranks).
+        """
+        k_pool, v_pool, page_table = kv
+        bounds, nsum, seq_len = seg
+        p = self.params
+        if close_items is not None and close_items.numel():
+            self.update_mean_keys(kv, seg, close_items)
+        if update_selection:
+            Z.score(self.shape, q, self.mean_keys, nsum, p.top_k, self.partial, self.alpha, self.topk,
+                    self.status)
+            if allreduce is not None:
+                allreduce(self.partial)
+            Z.select_topc(self.partial, nsum, p.c, self.flags, self.agreeability, self.status)
+        Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count,
+                      self.status)
+        Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
+                             self.out, self.workspace, dev_status=self.status)
+        return self.out
+
+    def launches_per_step(self, update_selection=True, close=False) -> int:
+        """Kernel launches one run() enqueues (a2 = zero + score)."""
+        return (1 if close else 0) + (3 if update_selection else 0) + 2
+
+    def capture(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None):
+        """Capture run() into a CUDA graph (one launch per step afterwards)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):  # warm-up outside the graph (sets kernel attributes)
+                self.run(q, kv, seg, update_selection, close_items, allreduce)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run(q, kv, seg, update_selection, close_items, allreduce)
+        return g
+
+    def check_status(self):
+        st = int(self.status.item())
+        if st:
+            raise Z.ZoomrError("device status", st)

@@ -1,0 +1,199 @@
+"""Thin Python binding of libzoomr.so (include/zoomr.h): argument marshalling only.
+
+Every function has the name of the C entry point without the ``zoomr_`` prefix,
+takes CUDA torch tensors (PyTorch supplies device memory and the stream) and
+enqueues the CUDA kernels on the current stream.  No arithmetic of the method
+runs here.  There is no fallback: if the library is missing or a tensor is not
+a CUDA tensor of the documented dtype/shape, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libzoomr.so")
+
+OK, ERR_INVALID_ARG, ERR_DIM_MISMATCH, ERR_EMPTY_SEGMENT, ERR_SEGMENT_ORDER, ERR_INDEX_RANGE, \
+    ERR_CAPACITY, ERR_UNSUPPORTED, ERR_CUDA, ERR_WORKSPACE = range(10)
+A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
+
+EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
+           "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_status_str",
+           "zoomr_abi_version")
+
+
+class ZoomrError(RuntimeError):
+    def __init__(self, fn, rc):
+        super().__init__(f"{fn}: {status_str(rc)} ({rc})")
+        self.rc = rc
+
+
+class Geom(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("page_size", C.c_int32)]
+
+
+class KV(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("num_pages", C.c_int64),
+                ("page_table", C.c_void_p), ("max_pages", C.c_int32)]
+
+
+class Segments(C.Structure):
+    _fields_ = [("bounds", C.c_void_p), ("num_summaries", C.c_void_p), ("seq_len", C.c_void_p),
+                ("max_summaries", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libzoomr.so; raise if it is absent (no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the CUDA extension is required; there is no fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+        L.zoomr_update_mean_keys.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp]
+        L.zoomr_score.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        L.zoomr_select_topc.argtypes = [i32, vp, vp, i32, i32, vp, vp, vp, vp]
+        L.zoomr_build_index.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]
+        L.zoomr_attn_workspace_bytes.argtypes = [vp, i32]
+        L.zoomr_attn_workspace_bytes.restype = sz
+        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, i32, C.c_float, vp, vp, sz,
+                                               vp, vp]
+        L.zoomr_status_str.argtypes = [C.c_int]
+        L.zoomr_status_str.restype = C.c_char_p
+        L.zoomr_abi_version.restype = C.c_int
+        for fn in (L.zoomr_update_mean_keys, L.zoomr_score, L.zoomr_select_topc,
+                   L.zoomr_build_index, L.zoomr_sparse_decode_attn):
+            fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def status_str(rc: int) -> str:
+    return lib().zoomr_status_str(int(rc)).decode()
+
+
+def abi_version() -> int:
+    return int(lib().zoomr_abi_version())
+
+
+def _ptr(t, dtype=None, name="tensor"):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _check(fn, rc):
+    if rc != OK:
+        raise ZoomrError(fn, rc)
+
+
+@dataclass
+class Shape:
+    """Rank-local model geometry (zoomr_geom)."""
+    num_layers: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    page_size: int
+
+    def c(self) -> Geom:
+        return Geom(self.num_layers, self.num_q_heads, self.num_kv_heads, self.head_dim,
+                    self.page_size)
+
+
+def _kv(k_pool, v_pool, page_table):
+    if k_pool.shape != v_pool.shape or k_pool.dim() != 5:
+        raise ValueError("k/v pools must be [L][num_pages][H_kv][P][d]")
+    return KV(_ptr(k_pool, torch.bfloat16, "k_pool"), _ptr(v_pool, torch.bfloat16, "v_pool"),
+              k_pool.shape[1], _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
+
+
+def _seg(bounds, num_summaries, seq_len):
+    return Segments(_ptr(bounds, torch.int32, "bounds"), _ptr(num_summaries, torch.int32, "num_summaries"),
+                    _ptr(seq_len, torch.int32, "seq_len"), bounds.shape[1])
+
+
+def update_mean_keys(shape: Shape, k_pool, v_pool, page_table, bounds, num_summaries, seq_len,
+                     items, mean_keys, dev_status=None, stream=None):
+    """a1 (zoomr_update_mean_keys). items: int32 [n][2] of (b, i)."""
+    g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
+    rc = lib().zoomr_update_mean_keys(C.byref(g), bounds.shape[0], C.byref(kv), C.byref(sg),
+                                      _ptr(items, torch.int32, "items"), items.shape[0],
+                                      _ptr(mean_keys, torch.float32, "mean_keys"),
+                                      _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_update_mean_keys", rc)
+
+
+def score(shape: Shape, q, mean_keys, num_summaries, top_k, partial, alpha_out=None, topk_out=None,
+          dev_status=None, stream=None):
+    """a2 (zoomr_score). partial: int64 [B][2][max_summaries]."""
+    g = shape.c()
+    rc = lib().zoomr_score(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
+                           _ptr(mean_keys, torch.float32, "mean_keys"),
+                           _ptr(num_summaries, torch.int32, "num_summaries"), partial.shape[2],
+                           int(top_k), _ptr(partial, torch.int64, "partial"),
+                           _ptr(alpha_out, torch.float32, "alpha_out"),
+                           _ptr(topk_out, torch.int32, "topk_out"),
+                           _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_score", rc)
+
+
+def select_topc(partial, num_summaries, c, flags, agreeability=None, dev_status=None, stream=None):
+    """a3 (zoomr_select_topc). flags: uint8 [B][max_summaries]."""
+    rc = lib().zoomr_select_topc(partial.shape[0], _ptr(partial, torch.int64, "partial"),
+                                 _ptr(num_summaries, torch.int32, "num_summaries"), partial.shape[2],
+                                 int(c), _ptr(flags, torch.uint8, "flags"),
+                                 _ptr(agreeability, torch.float32, "agreeability"),
+                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_select_topc", rc)
+
+
+def build_index(bounds, num_summaries, seq_len, flags, sink, window, index, index_count,
+                dev_status=None, stream=None):
+    """a4 (zoomr_build_index). index: int32 [B][capacity]; index_count int32 [B]."""
+    sg = _seg(bounds, num_summaries, seq_len)
+    rc = lib().zoomr_build_index(bounds.shape[0], C.byref(sg), _ptr(flags, torch.uint8, "flags"),
+                                 int(sink), int(window), _ptr(index, torch.int32, "index"),
+                                 index.shape[1], _ptr(index_count, torch.int32, "index_count"),
+                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_build_index", rc)
+
+
+def attn_workspace_bytes(shape: Shape, batch: int) -> int:
+    g = shape.c()
+    return int(lib().zoomr_attn_workspace_bytes(C.byref(g), int(batch)))
+
+
+def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out,
+                       workspace, softmax_scale=None, dev_status=None, stream=None):
+    """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
+    rc = lib().zoomr_sparse_decode_attn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
+                                        C.byref(kv), _ptr(index, torch.int32, "index"),
+                                        _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                        C.c_float(sc), _ptr(out, torch.float32, "out"),
+                                        _ptr(workspace, None, "workspace"), workspace.numel() *
+                                        workspace.element_size(),
+                                        _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_sparse_decode_attn", rc)

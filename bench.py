@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- ZoomR select + sparse-decode step on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload 8b16k]
+
+One "step" = one pass of the whole hot path over one batch of synthetic input:
+a1 mean-key update of the newest closed summary, a2 scoring + per-head top-k +
+vote aggregation, a3 global top-c, a4 index build, a5 sparse decode attention
+over I_f, for every layer and head (selection every step, U = 1).
+N = 1 runs BASELINE configs[1] (Llama-3-8B shape, 16K context, batch 1).  N > 1
+(launched by torchrun, one rank per GPU, NCCL) runs the same per-rank workload
+on every rank with no data-path collective ("scaling": "weak"); the step time
+is the max over ranks of the device-timed region.
+
+Prints ONE JSON line on rank 0 (bench contract in the task statement).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "select+sparse-decode step µs and seqs/s at 1/2/4/8 B200; % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="8b16k")
+    ap.add_argument("--query", default="planted", choices=["planted", "diffuse"])
+    ap.add_argument("--rotate", type=int, default=4, help="independent input sets cycled per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers --
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, counts, n_sum, closures=1):
+    """SURVEY 8(d) bytes_step, per rank, U = 1.
+
+    a5: |I_f| * L*H_kv*d*2*2 (K and V rows) + q read + fp32 out write + index read
+    a4: |I_f| * 4 index write
+    a2: N_t * L*H_kv*d*4 fp32 mean keys + q
+    a1: |S| * L*H_kv*d*2 + L*H_kv*d*4 for the newest closed summary
+    """
+    L, Hq, Hkv, d = cfg.L, cfg.Hq, cfg.Hkv, cfg.d
+    a5 = sum(c * L * Hkv * d * 4 + L * Hq * d * 2 + L * Hq * d * 4 + c * 4 for c in counts)
+    a4 = sum(c * 4 for c in counts)
+    a2 = sum(n * L * Hkv * d * 4 + L * Hq * d * 2 for n in n_sum)
+    a1 = closures * (cfg.LS * L * Hkv * d * 2 + L * Hkv * d * 4)
+    return {"a5": a5, "a4": a4, "a2": a2, "a1": a1, "total": a5 + a4 + a2 + a1}
+
+
+def init_dist(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return rank, world, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------- CPU oracle --
+def oracle_time(inp, seconds, threads=0):
+    """Time the CPU oracle (as it stands) on rank 0: full steps of sequence 0."""
+    import oracle
+    from zoomr_synth import bf16_bits, logical_rows
+    oracle.build()
+    cfg = inp.cfg
+    K = bf16_bits(logical_rows(inp, 0, "k"))
+    V = bf16_bits(logical_rows(inp, 0, "v"))
+    q = bf16_bits(inp.q[0])
+    n = int(inp.num_summaries[0])
+    seg = inp.bounds[0, :n].cpu().numpy()
+    nth = oracle.num_threads(threads)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.step(q, K, V, seg, cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.top_k, cfg.c, cfg.sink, cfg.window,
+                    threads=threads)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return steps, el, nth
+
+
+def run_reference(args):
+    rank, world, local = init_dist(args.gpus)
+    if rank != 0:
+        return
+    import zoomr_synth as S
+    cfg = S.CONFIGS[args.workload]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    inp = S.generate(cfg, device=dev, query_mode=args.query)
+    import oracle
+    from zoomr_synth import bf16_bits, logical_rows
+    oracle.build()
+    K = bf16_bits(logical_rows(inp, 0, "k"))
+    V = bf16_bits(logical_rows(inp, 0, "v"))
+    q = bf16_bits(inp.q[0])
+    n = int(inp.num_summaries[0])
+    seg = inp.bounds[0, :n].cpu().numpy()
+
+    def one():
+        return oracle.step(q, K, V, seg, cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.top_k, cfg.c, cfg.sink,
+                           cfg.window)
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = one()
+    el = time.perf_counter() - t0
+    val = args.steps * inp.q.shape[0] / el
+    cores = oracle.num_threads(0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "seqs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "batch": inp.q.shape[0], "T": cfg.T, "n_summaries": n,
+                   "index_count": int(len(r["index"])), "query": args.query},
+        "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle",
+                         "sample": f"full oracle step (a1-a5, all {cfg.L}x{cfg.Hq} heads) of one "
+                                   f"{cfg.name} sequence per step"},
+        "e2e": {"value": val, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm ----
+def run_ours(args):
+    rank, world, local = init_dist(args.gpus)
+    import zoomr_synth as S
+    from paper_2604_10898_b200 import _build
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.step import StepParams, ZoomrStep
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py (ours) needs a CUDA device")
+    _build.build()
+    cfg = S.CONFIGS[args.workload]
+    B = cfg.batch if args.workload != "8b32k" else cfg.batch
+    R = max(1, args.rotate)
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    prm = StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window)
+    sets = []
+    for r in range(R):
+        inp = S.generate(cfg, device="cuda", seed=cfg.seed + 1000 * rank + 17 * r, query_mode=args.query)
+        st = ZoomrStep(shape, inp.q.shape[0], inp.bounds.shape[1], cfg.T, prm)
+        kv = (inp.k_pool, inp.v_pool, inp.page_table)
+        seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+        st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))  # initial cache (untimed)
+        # the newest closed summary of every sequence: re-derived every step (a1 amortized)
+        newest = torch.tensor([[b, int(inp.num_summaries[b]) - 1] for b in range(inp.q.shape[0])],
+                              dtype=torch.int32, device="cuda")
+        g = st.capture(inp.q, kv, seg, update_selection=True, close_items=newest)
+        # a5 alone (for the kernel roofline), same buffers
+        ga = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ga):
+            Z.sparse_decode_attn(shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, st.index, st.count,
+                                 st.out, st.workspace, dev_status=st.status)
+        sets.append(dict(inp=inp, st=st, g=g, ga=ga, kv=kv, seg=seg, newest=newest))
+    torch.cuda.synchronize()
+    for s in sets:
+        s["st"].check_status()
+    launches = sets[0]["st"].launches_per_step(update_selection=True, close=True)
+    counts = [[int(c) for c in s["st"].count.cpu()] for s in sets]
+    nsum = [[int(n) for n in s["inp"].num_summaries.cpu()] for s in sets]
+    per_set_bytes = [algorithmic_bytes(cfg, counts[i], nsum[i]) for i in range(R)]
+
+    def timed(fn, K, W):
+        for i in range(W):
+            fn(i)
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(K):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        return e0.elapsed_time(e1) / 1e3  # s
+
+    K, W = args.steps, max(3, args.warmup)
+    clk = ClockSampler(local).__enter__()
+    time.sleep(1.0)  # let nvidia-smi start sampling before the timed region
+    t_step = timed(lambda i: sets[i % R]["g"].replay(), K, W)
+    if len(clk.rows) < 3:  # short run: keep the GPU busy with timed-equivalent replays while sampling
+        for _ in range(3):
+            timed(lambda i: sets[i % R]["g"].replay(), K, 0)
+    clk.__exit__()
+    t_step_max = max_over_ranks(t_step, world)
+    t_attn = timed(lambda i: sets[i % R]["ga"].replay(), K, W)
+    bytes_mean = sum(per_set_bytes[i % R]["total"] for i in range(K)) / K
+    a5_mean = sum(per_set_bytes[i % R]["a5"] for i in range(K)) / K
+    Bseq = sets[0]["inp"].q.shape[0]
+
+    # e2e through the public API: pinned host q in, fp32 out back to host, every step
+    qh = [s["inp"].q.cpu().pin_memory() for s in sets]
+    oh = [torch.empty_like(s["st"].out, device="cpu").pin_memory() for s in sets]
+
+    def e2e_step(i):
+        s = sets[i % R]
+        s["inp"].q.copy_(qh[i % R], non_blocking=True)
+        s["g"].replay()
+        oh[i % R].copy_(s["st"].out, non_blocking=True)
+    t_e2e = max_over_ranks(timed(e2e_step, K, W), world)
+    h2d = sets[0]["inp"].q.numel() * 2
+    d2h = sets[0]["st"].out.numel() * 4
+
+    # per-stage breakdown (informational): each stage alone, graph-replayed
+    stages = {}
+    s0 = sets[0]
+    st, inp = s0["st"], s0["inp"]
+    REP = 20  # launches per graph: the per-stage figure is GPU time, not CPU launch overhead
+
+    def cap(fn):
+        gg = torch.cuda.CUDAGraph()
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gg):
+            for _ in range(REP):
+                fn()
+        return gg
+    st_graphs = {
+        "a1_a4_fused_select": cap(lambda: Z.select_fused(
+            shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, inp.bounds, inp.num_summaries, inp.seq_len,
+            s0["newest"], st.mean_keys, cfg.top_k, cfg.c, cfg.sink, cfg.window, st.flags, st.index, st.count,
+            st.sel_workspace, partial=st.partial, agreeability=st.agreeability, dev_status=st.status)),
+        "a1_mean_keys": cap(lambda: st.update_mean_keys(s0["kv"], s0["seg"], s0["newest"])),
+        "a2_score": cap(lambda: Z.score(shape, inp.q, st.mean_keys, inp.num_summaries, cfg.top_k, st.partial,
+                                        dev_status=st.status)),
+        "a3_select_topc": cap(lambda: Z.select_topc(st.partial, inp.num_summaries, cfg.c, st.flags,
+                                                    st.agreeability, st.status)),
+        "a4_build_index": cap(lambda: Z.build_index(inp.bounds, inp.num_summaries, inp.seq_len, st.flags,
+                                                    cfg.sink, cfg.window, st.index, st.count, st.status)),
+    }
+    for k, gg in st_graphs.items():
+        stages[k] = round(timed(lambda i: gg.replay(), 10, 2) / (10 * REP) * 1e6, 2)
+    stages["a5_sparse_attn"] = round(t_attn / K * 1e6, 2)
+    torch.cuda.synchronize()
+    for s in sets:
+        s["st"].check_status()
+
+    hbm, peak_src = peaks()
+    step_s = t_step_max / K
+    value = world * Bseq * K / t_step_max
+    attn_s = t_attn / K
+    achieved = a5_mean / attn_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(cfg.name, {}).get("a5_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "seqs/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name, "batch_per_gpu": Bseq, "global_batch": Bseq * world, "T": cfg.T,
+                   "L": cfg.L, "H_q": cfg.Hq, "H_kv": cfg.Hkv, "d": cfg.d, "n_summaries": nsum[0][0],
+                   "c": cfg.c, "top_k": cfg.top_k, "sink": cfg.sink, "window": cfg.window,
+                   "update_every": 1, "query": args.query, "index_count_mean":
+                       sum(sum(c) for c in counts) / sum(len(c) for c in counts),
+                   "parallelism": f"batch-shard x{world}" if world > 1 else "single",
+                   "l2": f"inputs larger than L2: {R} independent input sets rotated per step, "
+                         f"each step reads {bytes_mean / 1e6:.0f} MB"},
+        "step_us": step_s * 1e6,
+        "step_roofline": {"bytes_per_step": bytes_mean, "achieved_gbs": bytes_mean / step_s / 1e9,
+                          "frac": bytes_mean / step_s / 1e9 / hbm},
+        "roofline": {"kernel": "a5 zoomr_sparse_decode_attn", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": a5_mean,
+                     "launch_us": attn_s * 1e6},
+        "stages_us": stages,
+        "e2e": {"value": world * Bseq * K / t_e2e, "unit": "seqs/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches * K,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        steps, el, nth = oracle_time(sets[0]["inp"], args.cpu_seconds)
+        line["cpu_baseline"] = {"value": steps * Bseq / el, "unit": "seqs/s", "cores": nth, "kind": "oracle",
+                                "sample": f"{steps} full oracle steps (a1-a5, all {cfg.L}x{cfg.Hq} heads) of "
+                                          f"one {cfg.name} sequence, {el:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -170,6 +170,31 @@ int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *
                              float softmax_scale, float *out, void *workspace,
                              size_t workspace_bytes, int32_t *dev_status, void *stream);
 
+/* a1 + a2 + a3 + a4 fused into ONE launch for the single-rank / batch-sharded
+ * step (Algorithm 1's selection).  Same semantics and bit-identical
+ * outputs as calling, in order,
+ *   zoomr_update_mean_keys(close_items) ; zoomr_score ; zoomr_select_topc ;
+ *   zoomr_build_index
+ * with the same arguments: each (layer, KV head) CTA recomputes the mean keys
+ * of the summaries in close_items (device int32 [n_close][2] of (b, i); may be
+ * empty) for its own (l, g), scores, and publishes its voters' top-k; the last
+ * CTA of each sequence aggregates (exact integer votes and fixed-point A),
+ * selects the consensus and writes the index set.  partial, agreeability,
+ * alpha_out and topk_out are optional outputs (nullable).  Not for the
+ * KV-head-sharded mode (no all-reduce point): use the separate calls there.
+ * workspace: >= zoomr_select_workspace_bytes(geom, batch, max_summaries) bytes of
+ * device memory, zero-filled once before the first call; every call leaves it
+ * ready for the next (its per-sequence tickets are reset). */
+size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t batch, int32_t max_summaries);
+
+int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                       const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                       float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
+                       int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
+                       int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                       int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                       int32_t *dev_status, void *stream);
+
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);
 

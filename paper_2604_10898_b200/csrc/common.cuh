@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/zoomr.h"
 
@@ -40,6 +41,19 @@ inline int num_sms() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
   }
   return n;
+}
+
+// Every libzoomr kernel asks for the maximum shared-memory carveout so that
+// consecutive kernels of a step never force an L1/shared re-partition of the
+// SMs (env ZOOMR_CARVEOUT=-1 disables, for A/B measurements).
+template <typename F>
+inline void prefer_max_smem(F *kfn) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char *e = getenv("ZOOMR_CARVEOUT");
+    mode = e ? atoi(e) : 100;
+  }
+  if (mode >= 0) cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, mode);
 }
 
 inline bool valid_geom(const zoomr_geom *g) {

@@ -6,17 +6,24 @@
 //
 // B200 design:
 //  * Work = the flattened sequence of 32-token tiles of every (b, l, g)
-//    segment.  A persistent grid (one CTA per SM) gives each consumer warp a
+//    segment.  A persistent grid (one CTA per SM) gives each math warp a
 //    contiguous, equal share of that sequence ("stream-K" split): perfect load
 //    balance whatever |I_f| turns out to be on the device, and at most two
 //    partial results per warp.  Segments split across warps are merged by the
 //    last-arriving warp (arrival counter per segment, self-resetting).
-//  * Gather: one producer warp per CTA turns I_f positions into paged row
-//    addresses (page table lookup) and issues one TMA bulk copy
-//    (cp.async.bulk, UBLKCP) per K row and per V row straight into a
-//    multi-stage shared-memory ring, completing on an mbarrier (expect_tx).
-//    Rows land at a 2*d+16 byte stride so the ldmatrix reads below are
-//    bank-conflict free.
+//  * Warp specialisation in producer/consumer PAIRS.  The gather address chain
+//    (I_f position -> page table -> row address: two dependent L2 loads) is
+//    decoupled from the math: producer warp p resolves tile k+1 while it copies
+//    tile k for math warp p, with 16-byte cp.async.cg (LDGSTS, L1 bypass; one
+//    warp instruction moves whole 256-byte rows, 16 lanes per row) into a
+//    kStages-deep ring of shared-memory tiles whose rows are padded to a
+//    2*d+16 byte stride (conflict-free ldmatrix).  Completion is signalled with
+//    cp.async.mbarrier.arrive.noinc on a per-stage mbarrier; the math warp frees
+//    the stage with a plain mbarrier arrive.  Rows past the end of a segment are
+//    zero-filled by the copy (src-size 0).  (Version 0 issued one TMA bulk copy
+//    per 256-byte row: ncu showed the producer issue-bound at ~90 cycles per
+//    copy -- profiles/r01_k5_v0_*; version 1 did gather and math in the same
+//    warp and was latency-bound -- profiles/r01_k5_v1_*.)
 //  * Math on tensor cores (mma.sync m16n8k16, bf16 in, fp32 accumulate):
 //      S^T-tile = K_tile (32 tok x d) . Q^T (d x 8 padded heads)
 //      O^T     += V_tile^T (d x 32 tok) . P (32 tok x 8)
@@ -31,17 +38,20 @@
 
 namespace zoomr {
 
-constexpr int kTile = 32;  // tokens per consumer tile (one per producer lane)
-constexpr int kNCW = 4;    // consumer warps per CTA
-constexpr int kNSW = 3;    // ring stages per consumer warp
+constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addresses)
+constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
+constexpr int kStages = 3;  // ring depth per pair
 
 template <int D>
 struct AttnShape {
-  static constexpr int RB = 2 * D;              // bytes of one K or V row (bf16)
-  static constexpr int RS = 2 * D + 16;         // padded smem row stride (conflict-free ldmatrix)
+  static constexpr int RB = 2 * D;               // bytes of one K or V row (bf16)
+  static constexpr int RS = 2 * D + 16;          // padded smem row stride (conflict-free ldmatrix)
+  static constexpr int CPR = RB / 16;            // 16-byte chunks per row
+  static constexpr int RPI = 32 / CPR;           // rows copied per warp instruction
   static constexpr int TILE_BYTES = kTile * RS;  // K (or V) part of a stage
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
-  static constexpr int RING_BYTES = kNCW * kNSW * STAGE_BYTES;
+  static constexpr int RING_BYTES = kPairs * kStages * STAGE_BYTES;
+  static constexpr int BAR_BYTES = 2 * kPairs * kStages * 8;
 };
 
 struct AttnParams {
@@ -55,20 +65,22 @@ struct AttnParams {
   const int32_t *count;
   int32_t cap;
   float *out;
-  float *ws_part;      // [NW][2][G*(D+2)]
-  int32_t *ws_cnt;     // [B*L*Hkv]
-  int32_t B, L, Hkv, P;
+  float *ws_part;  // [NW][2][G*(D+2)]
+  int32_t *ws_cnt; // [B*L*Hkv]
+  int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
   float scale_log2;
   int32_t *status;
 };
 
 // ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -82,11 +94,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
   } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -125,8 +132,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
 struct Sched {
   const int32_t *prefix;  // smem [B+1]: first global tile of sequence b
   int64_t T_tot;
-  int64_t NWe;            // effective number of warps (<= T_tot)
-  int32_t B, LH;          // LH = L * Hkv segments per sequence
+  int64_t NWe;  // effective number of math warps (<= T_tot)
+  int32_t B, LH;  // LH = L * Hkv segments per sequence
   __device__ __forceinline__ int64_t range_start(int64_t w) const { return T_tot * w / NWe; }
   __device__ __forceinline__ int64_t warp_of(int64_t t) const { return ((t + 1) * NWe - 1) / T_tot; }
   // global tile -> (b, segment within b, tile within segment, tiles per segment of b)
@@ -145,23 +152,23 @@ struct Sched {
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnParams p) {
   using S = AttnShape<D>;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kNCW][kNSW]
-  uint64_t *empty = full + kNCW * kNSW;                                 // [kNCW][kNSW]
-  int32_t *prefix = reinterpret_cast<int32_t *>(empty + kNCW * kNSW);   // [B+1]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kPairs][kStages]
+  uint64_t *empty = full + kPairs * kStages;                             // [kPairs][kStages]
+  int32_t *prefix = reinterpret_cast<int32_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // [B+1]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
 
   if (threadIdx.x == 0) {
-    for (int x = 0; x < kNCW * kNSW; ++x) {
-      mbar_init(&full[x], 1);
-      mbar_init(&empty[x], 1);
+    for (int x = 0; x < kPairs * kStages; ++x) {
+      mbar_init(&full[x], 32);  // one cp.async arrive (noinc) per producer lane
+      mbar_init(&empty[x], 1);  // the math warp's lane 0
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // tiles per sequence -> prefix (B is small; warp 0 scans in chunks of 32)
+  // tiles per sequence -> prefix (warp 0 scans in chunks of 32 sequences)
   if (warp == 0) {
     int carry = 0;
     for (int b0 = 0; b0 < p.B; b0 += 32) {
@@ -191,104 +198,87 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
   sc.B = p.B;
   sc.LH = p.L * p.Hkv;
   if (sc.T_tot == 0) return;
-  const int64_t NW = (int64_t)gridDim.x * kNCW;
+  const int64_t NW = (int64_t)gridDim.x * kPairs;
   sc.NWe = NW < sc.T_tot ? NW : sc.T_tot;
 
-  if (warp == kNCW) {
-    // ======================= producer: paged gather via TMA bulk copies =====
-    int64_t r0[kNCW], nt[kNCW];
-#pragma unroll
-    for (int w = 0; w < kNCW; ++w) {
-      const int64_t gw = (int64_t)blockIdx.x * kNCW + w;
-      if (gw < sc.NWe) {
-        r0[w] = sc.range_start(gw);
-        nt[w] = sc.range_start(gw + 1) - r0[w];
-      } else {
-        r0[w] = 0;
-        nt[w] = 0;
-      }
-    }
-    int64_t kmax = 0;
-#pragma unroll
-    for (int w = 0; w < kNCW; ++w) kmax = nt[w] > kmax ? nt[w] : kmax;
-    const uint32_t ring = smem_u32(smem);
-    for (int64_t k = 0; k < kmax; ++k) {
-      // phase 1: resolve this round's rows for every consumer warp (independent loads in flight)
-      const __nv_bfloat16 *ksrc[kNCW], *vsrc[kNCW];
-      int nvalid[kNCW];
-#pragma unroll
-      for (int w = 0; w < kNCW; ++w) {
-        ksrc[w] = nullptr;
-        vsrc[w] = nullptr;
-        nvalid[w] = 0;
-        if (k < nt[w]) {
-          int b, seg, tis, nts;
-          sc.locate(r0[w] + k, b, seg, tis, nts);
-          int cnt = p.count[b];
-          cnt = cnt < p.cap ? cnt : p.cap;
-          const int l = seg / p.Hkv, g = seg - l * p.Hkv;
-          const int pos0 = tis * kTile;
-          nvalid[w] = min(kTile, cnt - pos0);
-          if (lane < nvalid[w]) {
-            const int tok = p.index[(int64_t)b * p.cap + pos0 + lane];
-            const int lp = tok / p.P;
-            int page = 0;
-            if (tok >= 0 && lp < p.max_pages) page = p.page_table[(int64_t)b * p.max_pages + lp];
-            if (tok < 0 || lp >= p.max_pages || page < 0 || page >= p.num_pages) {
-              set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
-              page = 0;
-            }
-            const int64_t row = (((int64_t)l * p.num_pages + page) * p.Hkv + g) * p.P + (tok - lp * p.P);
-            ksrc[w] = p.kpool + row * D;
-            vsrc[w] = p.vpool + row * D;
-          }
+  const int pair = warp % kPairs;
+  const bool producer = warp >= kPairs;
+  const int64_t gw = (int64_t)blockIdx.x * kPairs + pair;  // global math-warp id of the pair
+  if (gw >= sc.NWe) return;
+  const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
+  const int64_t ntiles = r1 - r0;
+  const uint32_t ring = smem_u32(smem) + (uint32_t)(pair * kStages * S::STAGE_BYTES);
+  uint64_t *fullp = full + pair * kStages;
+  uint64_t *emptyp = empty + pair * kStages;
+
+  if (producer) {
+    // ================= producer: resolve rows one tile ahead, LDGSTS them ====
+    auto resolve = [&](int64_t k, const __nv_bfloat16 *&krow, const __nv_bfloat16 *&vrow, int &ok) {
+      int b, seg, tis, nts;
+      sc.locate(r0 + k, b, seg, tis, nts);
+      int cnt = p.count[b];
+      cnt = cnt < p.cap ? cnt : p.cap;
+      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      const int pos = tis * kTile + lane;
+      ok = pos < cnt;
+      krow = p.kpool;
+      vrow = p.vpool;
+      if (ok) {
+        const int tok = p.index[(int64_t)b * p.cap + pos];
+        const int lp = p.Pshift >= 0 ? (tok >> p.Pshift) : tok / p.P;
+        const int slot = tok - lp * p.P;
+        int page = 0;
+        if (tok >= 0 && lp < p.max_pages) page = p.page_table[(int64_t)b * p.max_pages + lp];
+        if (tok < 0 || lp >= p.max_pages || page < 0 || page >= p.num_pages) {
+          set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+          page = 0;
         }
+        const int64_t row = (((int64_t)l * p.num_pages + page) * p.Hkv + g) * p.P + slot;
+        krow = p.kpool + row * D;
+        vrow = p.vpool + row * D;
       }
-      // phase 2: claim the stage and launch the copies
+    };
+    const __nv_bfloat16 *ck = nullptr, *cv = nullptr, *nk = nullptr, *nv = nullptr;
+    int cok = 0, nok = 0;
+    if (ntiles > 0) resolve(0, ck, cv, cok);
+    const int rsub = lane / S::CPR, ch = lane % S::CPR;
+    for (int64_t k = 0; k < ntiles; ++k) {
+      if (k + 1 < ntiles) resolve(k + 1, nk, nv, nok);  // loads overlap the wait + copies below
+      const int s = (int)(k % kStages);
+      mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1));
+      const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
+      const uint32_t stV = stK + S::TILE_BYTES;
 #pragma unroll
-      for (int w = 0; w < kNCW; ++w) {
-        if (k >= nt[w]) continue;
-        const int s = (int)(k % kNSW);
-        const uint32_t par = (uint32_t)((k / kNSW) & 1);
-        mbar_wait(&empty[w * kNSW + s], par ^ 1u);
-        const uint32_t stK = ring + (uint32_t)((w * kNSW + s) * S::STAGE_BYTES);
-        const uint32_t stV = stK + S::TILE_BYTES;
-        if (lane >= nvalid[w]) {
-          // rows past the end of the segment: zero V so that P = 0 cannot meet stale NaNs
-          uint4 *vr = reinterpret_cast<uint4 *>(smem + (stV - ring) + lane * S::RS);
-#pragma unroll
-          for (int x = 0; x < S::RB / 16; ++x) vr[x] = make_uint4(0, 0, 0, 0);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&full[w * kNSW + s], (uint32_t)(nvalid[w] * 2 * S::RB));
-        __syncwarp();
-        if (lane < nvalid[w]) {
-          bulk_g2s(stK + lane * S::RS, ksrc[w], S::RB, &full[w * kNSW + s]);
-          bulk_g2s(stV + lane * S::RS, vsrc[w], S::RB, &full[w * kNSW + s]);
-        }
+      for (int i = 0; i < kTile / S::RPI; ++i) {
+        const int r = i * S::RPI + rsub;  // token row of this lane's chunk
+        const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
+        const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
+        const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;  // 0: zero-fill past the end
+        cp_async16(stK + r * S::RS + ch * 16, kr + ch * 8, n);
+        cp_async16(stV + r * S::RS + ch * 16, vr + ch * 8, n);
       }
+      cp_async_arrive_noinc(&fullp[s]);
+      ck = nk;
+      cv = nv;
+      cok = nok;
     }
     return;
   }
 
-  // ========================= consumers: tensor-core flash-decode ============
-  const int64_t gw = (int64_t)blockIdx.x * kNCW + warp;
-  if (gw >= sc.NWe) return;
-  const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
+  // ====================== math warp: tensor-core flash-decode ==============
   const int gq = lane >> 2, tq = lane & 3;  // mma fragment row group / thread-in-group
   const int n0 = 2 * tq;                    // the two MMA columns this thread holds: n0, n0+1
   constexpr int NKS = D / 16;               // k-steps of QK^T and m-tiles of O^T
   constexpr bool kTwoN = (G == 8);          // hi and lo in separate n-tiles
   // column -> (head, part) for G <= 4: head = n % G, part = n / G (0 hi, 1 lo, >=2 none)
   const int part0 = kTwoN ? 0 : n0 / G, part1 = kTwoN ? 0 : (n0 + 1) / G;
+  constexpr int SLOT = G * (D + 2);  // partial result: m[G], l[G], O[G][D]
 
   int first_b = -1, first_seg = -1;  // the first segment of this warp's range (slot rule)
   int cur_b = -1, cur_seg = -1;
   uint32_t qf[NKS][2];
   float o[NKS][4], o2[kTwoN ? NKS : 1][4];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  const uint32_t ring = smem_u32(smem);
 
   auto flush = [&](int b, int seg) {
     // finish the segment's softmax state and publish it (final or partial)
@@ -322,10 +312,10 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
     const int nts = (sc.prefix[b + 1] - sc.prefix[b]) / sc.LH;
     const int64_t st0 = sc.prefix[b] + (int64_t)seg * nts, st1 = st0 + nts;
     const int64_t wf = sc.warp_of(st0), wl = sc.warp_of(st1 - 1);
+    float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
     if (wf == wl) {  // this warp owns the whole segment: final output
       if (owner) {
         const float inv0 = 1.f / l0, inv1 = 1.f / l1;
-        float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
 #pragma unroll
         for (int me = 0; me < NKS; ++me) {
           const int e = me * 16 + gq;
@@ -340,7 +330,6 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
       return;
     }
     // partial: slot 0 if this is the warp's first segment, else slot 1
-    constexpr int SLOT = G * (D + 2);
     const int slot = (b == first_b && seg == first_seg) ? 0 : 1;
     float *ps = p.ws_part + ((int64_t)gw * 2 + slot) * SLOT;
     if (owner) {
@@ -371,33 +360,70 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != (int)(wl - wf)) return;  // not the last arriving warp
     __threadfence();
-    // last arriver: merge the partials of warps wf..wl in order
-    for (int x = lane; x < G * D; x += 32) {
-      const int h = x / D, e = x - h * D;
-      float M = -INFINITY;
-      for (int64_t w2 = wf; w2 <= wl; ++w2) {
+    // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic)
+    const int nparts = (int)(wl - wf + 1);
+    float Mh[G], Lh[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) Mh[h] = -INFINITY;
+    // pass 1 (lane-parallel over parts): per-head max
+    for (int j0 = 0; j0 < nparts; j0 += 32) {
+      const int j = j0 + lane;
+      if (j < nparts) {
         int fb, fs, ft, fn;
-        sc.locate(sc.range_start(w2), fb, fs, ft, fn);
-        const int sl = (fb == b && fs == seg) ? 0 : 1;
-        const float *q2 = p.ws_part + (w2 * 2 + sl) * SLOT;
-        M = fmaxf(M, __ldcg(q2 + h));
+        sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
+        const float *q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
+#pragma unroll
+        for (int h = 0; h < G; ++h) Mh[h] = fmaxf(Mh[h], __ldcg(q2 + h));
       }
-      float Lsum = 0.f, Osum = 0.f;
-      for (int64_t w2 = wf; w2 <= wl; ++w2) {
-        int fb, fs, ft, fn;
-        sc.locate(sc.range_start(w2), fb, fs, ft, fn);
-        const int sl = (fb == b && fs == seg) ? 0 : 1;
-        const float *q2 = p.ws_part + (w2 * 2 + sl) * SLOT;
-        const float sc2 = ex2(__ldcg(q2 + h) - M);
-        Lsum += __ldcg(q2 + G + h) * sc2;
-        Osum += __ldcg(q2 + 2 * G + h * D + e) * sc2;
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+#pragma unroll
+      for (int off = 16; off; off >>= 1) Mh[h] = fmaxf(Mh[h], __shfl_xor_sync(0xffffffffu, Mh[h], off));
+    // pass 2: rescaled sums; lane-parallel over float4 of O[G][D]
+    constexpr int NV4 = G * D / 4;
+    constexpr int PER = (NV4 + 31) / 32;
+    float4 acc[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int h = 0; h < G; ++h) Lh[h] = 0.f;
+    for (int j = 0; j < nparts; ++j) {
+      int fb, fs, ft, fn;
+      sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
+      const float *q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
+      float w[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        w[h] = ex2(__ldcg(q2 + h) - Mh[h]);
+        Lh[h] += __ldcg(q2 + G + h) * w[h];
       }
-      p.out[(((int64_t)b * p.L + l) * Hq + (int64_t)g * G + h) * D + e] = Osum / Lsum;
+      const float *O = q2 + 2 * G;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int f = lane + 32 * u;
+        if (f < NV4) {
+          const float ww = w[(4 * f) / D];
+          acc[u].x += __ldcg(O + 4 * f + 0) * ww;
+          acc[u].y += __ldcg(O + 4 * f + 1) * ww;
+          acc[u].z += __ldcg(O + 4 * f + 2) * ww;
+          acc[u].w += __ldcg(O + 4 * f + 3) * ww;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int f = lane + 32 * u;
+      if (f < NV4) {
+        const float inv = 1.f / Lh[(4 * f) / D];
+        reinterpret_cast<float4 *>(ob)[f] =
+            make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
+      }
     }
     if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
   };
 
-  for (int64_t k = 0; r0 + k < r1; ++k) {
+  for (int64_t k = 0; k < ntiles; ++k) {
     int b, seg, tis, nts;
     sc.locate(r0 + k, b, seg, tis, nts);
     if (k == 0) {
@@ -429,9 +455,9 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
     int cnt = p.count[b];
     cnt = cnt < p.cap ? cnt : p.cap;
     const int nvalid = min(kTile, cnt - tis * kTile);
-    const int s = (int)(k % kNSW);
-    mbar_wait(&full[warp * kNSW + s], (uint32_t)((k / kNSW) & 1));
-    const uint32_t stK = ring + (uint32_t)((warp * kNSW + s) * S::STAGE_BYTES);
+    const int s = (int)(k % kStages);
+    mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
+    const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
     const uint32_t stV = stK + S::TILE_BYTES;
 
     // ---- S = K . Q^T  (2 m-tiles of 16 tokens) ----
@@ -520,22 +546,22 @@ __global__ void __launch_bounds__(32 * (kNCW + 1), 1) sparse_attn_kernel(const A
         if constexpr (kTwoN) mma_bf16(o2[me], a0, a1, a2, a3, bl[kt][0], bl[kt][1]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[warp * kNSW + s]);
+    __syncwarp();  // every lane is done reading the stage
+    if (lane == 0) mbar_arrive(&emptyp[s]);
   }
   if (cur_b >= 0) flush(cur_b, cur_seg);
 }
 
 template <int D, int G>
 size_t attn_smem_bytes(int B) {
-  return (size_t)AttnShape<D>::RING_BYTES + 2 * kNCW * kNSW * sizeof(uint64_t) + (size_t)(B + 1) * sizeof(int32_t);
+  return (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)(B + 1) * sizeof(int32_t);
 }
 
 inline int attn_grid() { return num_sms(); }
 
 inline size_t attn_ws_part_floats(const zoomr_geom *g) {
   const int G = g->num_q_heads / g->num_kv_heads;
-  return (size_t)attn_grid() * kNCW * 2 * G * (g->head_dim + 2);
+  return (size_t)attn_grid() * kPairs * 2 * G * (g->head_dim + 2);
 }
 
 }  // namespace zoomr
@@ -580,25 +606,29 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   prm.L = geom->num_layers;
   prm.Hkv = geom->num_kv_heads;
   prm.P = geom->page_size;
+  prm.Pshift = -1;
+  for (int sft = 0; sft < 31; ++sft)
+    if ((1 << sft) == geom->page_size) prm.Pshift = sft;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
   prm.status = dev_status;
   const int G = geom->num_q_heads / geom->num_kv_heads;
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = attn_grid();
-#define ZOOMR_AT(DD, GG)                                                                             \
-  do {                                                                                               \
-    auto kfn = sparse_attn_kernel<DD, GG>;                                                           \
-    const size_t smem = attn_smem_bytes<DD, GG>(batch);                                              \
-    if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                             \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);               \
-    kfn<<<grid, 32 * (kNCW + 1), smem, s>>>(prm);                                                    \
+#define ZOOMR_AT(DD, GG)                                                                 \
+  do {                                                                                   \
+    auto kfn = sparse_attn_kernel<DD, GG>;                                               \
+    const size_t smem = attn_smem_bytes<DD, GG>(batch);                                  \
+    if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                 \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    prefer_max_smem(kfn);                                                                \
+    kfn<<<grid, 64 * kPairs, smem, s>>>(prm);                                            \
   } while (0)
-#define ZOOMR_AT_G(DD)                 \
-  switch (G) {                         \
-    case 1: ZOOMR_AT(DD, 1); break;    \
-    case 2: ZOOMR_AT(DD, 2); break;    \
-    case 4: ZOOMR_AT(DD, 4); break;    \
-    default: ZOOMR_AT(DD, 8); break;   \
+#define ZOOMR_AT_G(DD)               \
+  switch (G) {                       \
+    case 1: ZOOMR_AT(DD, 1); break;  \
+    case 2: ZOOMR_AT(DD, 2); break;  \
+    case 4: ZOOMR_AT(DD, 4); break;  \
+    default: ZOOMR_AT(DD, 8); break; \
   }
   switch (geom->head_dim) {
     case 16: ZOOMR_AT_G(16); break;

@@ -1,0 +1,275 @@
+// zoomr_select_fused -- a1 + a2 + a3 + a4 of one decode step in ONE launch.
+//
+// Algorithm 1's per-step selection has a natural all-to-one shape:
+// every (layer, KV head) scores independently (a1, a2), then one consensus per
+// sequence (a3) decides the index set (a4).  The standalone kernels express that
+// with four launches and a global reduction through memory; on B200 at batch 1
+// each launch boundary and each dependent round trip costs microseconds against
+// a ~60 us step, so this kernel keeps the same building blocks
+// (select_common.cuh) but chains them with a last-CTA-arrives handoff:
+//   * CTA (l, g, b): recompute the mean key of every summary of b that closed
+//     this step (a1, block_mean_key), score all N_t mean keys against the G
+//     queries and take each voter's top-k (a2, block_score_topk), and add its
+//     G*k votes to per-sequence accumulators in the workspace with integer
+//     atomics at L2 -- votes and A = sum round(alpha*2^32), exact and
+//     order-independent (reading Q2);
+//   * the last CTA of sequence b to arrive (atomic ticket) reads the
+//     aggregate (and zeroes the accumulators for the next call), runs the
+//     consensus top-c (a3, block_topc) and builds I_f (a4, block_build_index),
+//     writing partial / flags / index / count, and resets its ticket.
+// (A first version published the picks and aggregated them in the last CTA
+// with shared-memory atomics: the consensus votes concentrate on a few
+// summaries, and the 64-bit shared atomic is a CAS loop -- 17 us of
+// serialisation; L2 integer atomics spread over the CTAs' lifetimes cost ~0.)
+// Results are bit-identical to the standalone chain (same arithmetic, integer
+// aggregation).  Single-rank only: the KV-head-sharded mode needs the
+// all-reduce between a2 and a3 and uses the standalone entry points.
+#include "select_common.cuh"
+
+namespace zoomr {
+
+
+struct FusedParams {
+  const __nv_bfloat16 *q;
+  const __nv_bfloat16 *kpool;
+  int64_t num_pages;
+  const int32_t *page_table;
+  int32_t max_pages;
+  const int32_t *bounds;
+  const int32_t *num_summaries;
+  const int32_t *seq_len;
+  int32_t max_summaries;
+  const int32_t *items;
+  int32_t n_items;
+  float *mean_keys;
+  int32_t top_k, c, sink, window;
+  int64_t *partial;       // nullable
+  uint8_t *flags;
+  float *agreeability;    // nullable
+  int32_t *index;
+  int32_t cap;
+  int32_t *count;
+  float *alpha_out;       // nullable
+  int32_t *topk_out;      // nullable
+  int32_t *ws_votes;      // [B][MS]  accumulators, zero between calls
+  long long *ws_a;        // [B][MS]
+  int32_t *ws_ticket;     // [B]
+  int32_t L, Hkv, P;
+  int32_t *status;
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int ticket_last;
+  const int lg = blockIdx.x, b = blockIdx.y;
+  const int l = lg / p.Hkv, g = lg - l * p.Hkv;
+  const int Hq = p.Hkv * G, V = p.L * Hq, MS = p.max_summaries;
+  int nt = p.num_summaries[b];
+  if (nt > MS || nt < 0) {
+    if (threadIdx.x == 0) set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+    nt = nt < 0 ? 0 : MS;
+  }
+  const int T = p.seq_len[b];
+  const int32_t *bd = p.bounds + (int64_t)b * MS * 4;
+  float *mk = p.mean_keys + (((int64_t)b * p.L + l) * p.Hkv + g) * (int64_t)MS * D;
+
+  // ---- a1: mean keys of the summaries of b that closed this step -----------
+  {
+    double *red = reinterpret_cast<double *>(smem_raw);  // [nwarps][D]
+    for (int it = 0; it < p.n_items; ++it) {
+      if (p.items[2 * it] != b) continue;
+      const int i = p.items[2 * it + 1];
+      if (i < 0 || i >= nt) {
+        if (threadIdx.x == 0) set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+        continue;
+      }
+      const int s0 = bd[4 * i + 2], s1 = bd[4 * i + 3];
+      if (s1 <= s0 || s0 < 0 || s1 > T) {
+        if (threadIdx.x == 0) set_status(p.status, s1 <= s0 ? ZOOMR_ERR_EMPTY_SEGMENT : ZOOMR_ERR_INDEX_RANGE);
+        continue;
+      }
+      block_mean_key<D>(p.kpool, p.num_pages, p.page_table + (int64_t)b * p.max_pages, p.max_pages, p.P, p.Hkv,
+                        l, g, s0, s1, red, mk + (int64_t)i * D, p.status);
+    }
+    __syncthreads();  // this CTA's own global writes are visible to it after the barrier
+  }
+
+  // ---- a2: alpha + per-voter top-k ----------------------------------------------
+  {
+    float *qs = reinterpret_cast<float *>(smem_raw);                 // [G][D]
+    float *al = qs + G * D;                                          // [G][MS]
+    int *sel_i = reinterpret_cast<int *>(al + G * MS);               // [G][k]
+    float *sel_a = reinterpret_cast<float *>(sel_i + G * p.top_k);   // [G][k]
+    const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
+    float *ao = p.alpha_out ? p.alpha_out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * MS : nullptr;
+    block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
+    const int kk = p.top_k < nt ? p.top_k : nt;
+    for (int x = threadIdx.x; x < G * p.top_k; x += blockDim.x) {
+      const int hh = x / p.top_k, r = x - hh * p.top_k;
+      const int64_t voter = (int64_t)l * Hq + g * G + hh;
+      if (r < kk) {  // votes and fixed-point A: integer atomics at L2, order-independent
+        atomicAdd(&p.ws_votes[(int64_t)b * MS + sel_i[x]], 1);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&p.ws_a[(int64_t)b * MS + sel_i[x]]),
+                  (unsigned long long)alpha_fixed(sel_a[x]));
+      }
+      if (p.topk_out) p.topk_out[((int64_t)b * V + voter) * p.top_k + r] = r < kk ? sel_i[x] : -1;
+    }
+  }
+  // ---- ticket: the last CTA of sequence b carries on --------------------------
+  // bar.sync orders the CTA's writes before thread 0's acq_rel ticket (release,
+  // cumulative at gpu scope); the winner's acquire + bar.sync order its reads after.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ws_ticket + b) : "memory");
+    ticket_last = (old == (unsigned)(p.L * p.Hkv - 1));
+  }
+  __syncthreads();
+  if (!ticket_last) return;
+
+  // ---- aggregation (a2, cross-head / cross-layer), exact integer atomics --------
+  SmemCarve sm{smem_raw};
+  long long *A = sm.take<long long>(MS);
+  int *v = sm.take<int>(MS);
+  int *grp = sm.take<int>(2 * MS);      // a3 tie group, then a4 pieces
+  int *hist = sm.take<int>(kHistBins);
+  int *scratch = sm.take<int>(40);
+  int4 *bds = sm.take<int4>(MS);        // segment table of b
+  uint8_t *fl = sm.take<uint8_t>(MS);
+  // collect the aggregate (leaving the accumulators zeroed for the next call)
+  // and stage the segment table for a4
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    bds[i] = reinterpret_cast<const int4 *>(bd)[i];
+    v[i] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
+    A[i] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
+    p.ws_votes[(int64_t)b * MS + i] = 0;
+    p.ws_a[(int64_t)b * MS + i] = 0;
+  }
+  __syncthreads();
+  if (p.partial) {
+    int64_t *pv = p.partial + (int64_t)b * 2 * MS;
+    for (int i = threadIdx.x; i < MS; i += blockDim.x) {
+      pv[i] = i < nt ? v[i] : 0;
+      pv[MS + i] = i < nt ? A[i] : 0;
+    }
+  }
+  // ---- a3: consensus top-c ----------------------------------------------------------
+  block_topc(v, A, nt, p.c, fl, hist, grp, scratch, p.agreeability ? p.agreeability + b : nullptr);
+
+  uint8_t *fo = p.flags + (int64_t)b * MS;
+  for (int i = threadIdx.x; i < MS; i += blockDim.x) fo[i] = i < nt ? fl[i] : 0;
+  __syncthreads();
+  // ---- a4: the index set --------------------------------------------------------------
+  if (T < 1) {
+    if (threadIdx.x == 0) {
+      set_status(p.status, ZOOMR_ERR_INVALID_ARG);
+      p.count[b] = 0;
+    }
+  } else {
+    block_build_index(reinterpret_cast<const int32_t *>(bds), nt, T, fl, p.sink, p.window, p.index + (int64_t)b * p.cap, p.cap, p.count + b, grp,
+                      scratch, p.status);
+  }
+  if (threadIdx.x == 0) p.ws_ticket[b] = 0;  // ready for the next step
+  __syncthreads();
+}
+
+template <int D, int G>
+size_t fused_smem_bytes(int MS, int top_k) {
+  const size_t a1 = 8 * (256 / 32) * D;
+  const size_t a2 = (size_t)G * D * 4 + (size_t)G * MS * 4 + (size_t)G * top_k * 8;
+  const size_t a3 = (size_t)MS * (8 + 4 + 8 + 16 + 1) + (kHistBins + 40) * 4 + 8 * 16;
+  return a1 > a2 ? (a1 > a3 ? a1 : a3) : (a2 > a3 ? a2 : a3);
+}
+
+}  // namespace zoomr
+
+using namespace zoomr;
+
+extern "C" size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t batch, int32_t max_summaries) {
+  if (check_geom(geom) || batch < 1 || max_summaries < 1) return 0;
+  return (size_t)batch * max_summaries * (8 + 4) + (size_t)batch * 4 + 256;
+}
+
+extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                                  const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                                  float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
+                                  int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
+                                  int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                                  int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                                  int32_t *dev_status, void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !q || !kv || !kv->k || !kv->page_table || !seg || !seg->bounds || !seg->num_summaries ||
+      !seg->seq_len || !mean_keys || !flags || !index || !index_count || index_capacity < 1 || top_k < 1 ||
+      c < 0 || sink < 0 || window < 1 || n_close < 0 || (n_close > 0 && !close_items) || !workspace ||
+      seg->max_summaries < 1 || kv->num_pages < 1 || kv->max_pages < 1)
+    return ZOOMR_ERR_INVALID_ARG;
+  if (top_k > kMaxTopK || seg->max_summaries > kMaxSummaries) return ZOOMR_ERR_UNSUPPORTED;
+  if (workspace_bytes < zoomr_select_workspace_bytes(geom, batch, seg->max_summaries)) return ZOOMR_ERR_WORKSPACE;
+  FusedParams p;
+  p.q = (const __nv_bfloat16 *)q;
+  p.kpool = (const __nv_bfloat16 *)kv->k;
+  p.num_pages = kv->num_pages;
+  p.page_table = kv->page_table;
+  p.max_pages = kv->max_pages;
+  p.bounds = seg->bounds;
+  p.num_summaries = seg->num_summaries;
+  p.seq_len = seg->seq_len;
+  p.max_summaries = seg->max_summaries;
+  p.items = close_items;
+  p.n_items = n_close;
+  p.mean_keys = mean_keys;
+  p.top_k = top_k;
+  p.c = c;
+  p.sink = sink;
+  p.window = window;
+  p.partial = partial;
+  p.flags = flags;
+  p.agreeability = agreeability;
+  p.index = index;
+  p.cap = index_capacity;
+  p.count = index_count;
+  p.alpha_out = alpha_out;
+  p.topk_out = topk_out;
+  const size_t nacc = (size_t)batch * seg->max_summaries;
+  p.ws_a = (long long *)workspace;
+  p.ws_votes = (int32_t *)((char *)workspace + nacc * 8);
+  p.ws_ticket = (int32_t *)((char *)workspace + nacc * 12);
+  p.L = geom->num_layers;
+  p.Hkv = geom->num_kv_heads;
+  p.P = geom->page_size;
+  p.status = dev_status;
+  const int G = geom->num_q_heads / geom->num_kv_heads;
+  dim3 grid(geom->num_layers * geom->num_kv_heads, batch);
+  cudaStream_t s = (cudaStream_t)stream;
+#define ZOOMR_FS(DD, GG)                                                                         \
+  do {                                                                                           \
+    auto kfn = fused_select_kernel<DD, GG>;                                                      \
+    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k);                     \
+    if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    prefer_max_smem(kfn);                                                                        \
+    kfn<<<grid, 256, smem, s>>>(p);                                                              \
+  } while (0)
+#define ZOOMR_FS_G(DD)               \
+  switch (G) {                       \
+    case 1: ZOOMR_FS(DD, 1); break;  \
+    case 2: ZOOMR_FS(DD, 2); break;  \
+    case 4: ZOOMR_FS(DD, 4); break;  \
+    default: ZOOMR_FS(DD, 8); break; \
+  }
+  switch (geom->head_dim) {
+    case 16: ZOOMR_FS_G(16); break;
+    case 32: ZOOMR_FS_G(32); break;
+    case 64: ZOOMR_FS_G(64); break;
+    default: ZOOMR_FS_G(128); break;
+  }
+#undef ZOOMR_FS_G
+#undef ZOOMR_FS
+  return launch_status();
+}
+
+extern "C" int zoomr_debug_timestamps(unsigned long long *out) {
+  return cudaMemcpyFromSymbol(out, zoomr::g_dbg_ts, sizeof(zoomr::g_dbg_ts)) == cudaSuccess ? 0 : 8;
+}

@@ -43,6 +43,8 @@ class ZoomrStep:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         ws = Z.attn_workspace_bytes(shape, batch)
         self.workspace = torch.zeros(max(ws, 1), dtype=torch.uint8, device=dev)
+        ws2 = Z.select_workspace_bytes(shape, batch, max_summaries)
+        self.sel_workspace = torch.zeros(max(ws2, 1), dtype=torch.uint8, device=dev)
         self.alpha = self.topk = None
         if debug_outputs:
             self.alpha = torch.zeros(batch, L, Hq, max_summaries, dtype=torch.float32, device=dev)
@@ -66,7 +68,7 @@ class ZoomrStep:
 
     # -- the step ----------------------------------------------------------------
     def run(self, q, kv, seg, update_selection: bool = True, close_items: Optional[torch.Tensor] = None,
-            allreduce: Optional[Callable[[torch.Tensor], None]] = None):
+            allreduce: Optional[Callable[[torch.Tensor], None]] = None, fused: bool = True):
         """Enqueue one decode step on the current stream.
 
         close_items: summaries that closed since the last step (a1, amortized).
@@ -77,6 +79,17 @@ class ZoomrStep:
         k_pool, v_pool, page_table = kv
         bounds, nsum, seq_len = seg
         p = self.params
+        if fused and update_selection and allreduce is None:
+            # a1..a4 in one launch (zoomr_select_fused), then a5
+            Z.select_fused(self.shape, q, k_pool, v_pool, page_table, bounds, nsum, seq_len,
+                           close_items if close_items is not None and close_items.numel() else None,
+                           self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags, self.index,
+                           self.count, self.sel_workspace, partial=self.partial,
+                           agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
+                           dev_status=self.status)
+            Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
+                                 self.out, self.workspace, dev_status=self.status)
+            return self.out
         if close_items is not None and close_items.numel():
             self.update_mean_keys(kv, seg, close_items)
         if update_selection:
@@ -91,21 +104,23 @@ class ZoomrStep:
                              self.out, self.workspace, dev_status=self.status)
         return self.out
 
-    def launches_per_step(self, update_selection=True, close=False) -> int:
-        """Kernel launches one run() enqueues (a2 = zero + score)."""
+    def launches_per_step(self, update_selection=True, close=False, fused=True) -> int:
+        """Kernel launches one run() enqueues (a2 = zero + score when not fused)."""
+        if fused and update_selection:
+            return 2
         return (1 if close else 0) + (3 if update_selection else 0) + 2
 
-    def capture(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None):
+    def capture(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=True):
         """Capture run() into a CUDA graph (one launch per step afterwards)."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(2):  # warm-up outside the graph (sets kernel attributes)
-                self.run(q, kv, seg, update_selection, close_items, allreduce)
+                self.run(q, kv, seg, update_selection, close_items, allreduce, fused)
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.run(q, kv, seg, update_selection, close_items, allreduce)
+            self.run(q, kv, seg, update_selection, close_items, allreduce, fused)
         return g
 
     def check_status(self):

@@ -22,8 +22,8 @@ OK, ERR_INVALID_ARG, ERR_DIM_MISMATCH, ERR_EMPTY_SEGMENT, ERR_SEGMENT_ORDER, ERR
 A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
 
 EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
-           "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_status_str",
-           "zoomr_abi_version")
+           "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
+           "zoomr_select_fused", "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -67,6 +67,11 @@ def lib():
         L.zoomr_attn_workspace_bytes.restype = sz
         L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, i32, C.c_float, vp, vp, sz,
                                                vp, vp]
+        L.zoomr_select_workspace_bytes.argtypes = [vp, i32, i32]
+        L.zoomr_select_workspace_bytes.restype = sz
+        L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp,
+                                         vp, i32, vp, vp, vp, vp, sz, vp, vp]
+        L.zoomr_select_fused.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -197,3 +202,27 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
                                         workspace.element_size(),
                                         _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_sparse_decode_attn", rc)
+
+
+def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:
+    g = shape.c()
+    return int(lib().zoomr_select_workspace_bytes(C.byref(g), int(batch), int(max_summaries)))
+
+
+def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summaries, seq_len, close_items,
+                 mean_keys, top_k, c, sink, window, flags, index, index_count, workspace, partial=None,
+                 agreeability=None, alpha_out=None, topk_out=None, dev_status=None, stream=None):
+    """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None."""
+    g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
+    n_close = 0 if close_items is None else close_items.shape[0]
+    rc = lib().zoomr_select_fused(
+        C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv), C.byref(sg),
+        _ptr(close_items, torch.int32, "close_items") if n_close else None, n_close,
+        _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k), int(c), int(sink), int(window),
+        _ptr(partial, torch.int64, "partial"), _ptr(flags, torch.uint8, "flags"),
+        _ptr(agreeability, torch.float32, "agreeability"), _ptr(index, torch.int32, "index"), index.shape[1],
+        _ptr(index_count, torch.int32, "index_count"), _ptr(alpha_out, torch.float32, "alpha_out"),
+        _ptr(topk_out, torch.int32, "topk_out"), _ptr(workspace, None, "workspace"),
+        workspace.numel() * workspace.element_size(), _ptr(dev_status, torch.int32, "dev_status"),
+        _stream(stream))
+    _check("zoomr_select_fused", rc)

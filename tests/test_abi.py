@@ -1,0 +1,64 @@
+"""CPU-side checks of the C-ABI boundary: the library loads without a GPU and
+exports every entry point include/zoomr.h declares; host-detectable argument
+errors are reported without touching a device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "zoomr.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(zoomr_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2604_10898_b200 import _build
+    path = _build.build()
+    return C.CDLL(path)
+
+
+def test_header_declares_the_five_stages():
+    fns = declared_functions()
+    for f in ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
+              "zoomr_sparse_decode_attn"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for f in declared_functions():
+        assert hasattr(lib, f), f"libzoomr.so does not export {f}"
+
+
+def test_binding_names_match_header():
+    from paper_2604_10898_b200 import zoomr as Z
+    assert set(Z.EXPORTS) == set(declared_functions())
+
+
+def test_status_strings_and_version(lib):
+    lib.zoomr_status_str.restype = C.c_char_p
+    assert lib.zoomr_status_str(0) == b"ZOOMR_OK"
+    assert lib.zoomr_status_str(6) == b"ZOOMR_ERR_CAPACITY"
+    assert lib.zoomr_status_str(999) == b"ZOOMR_ERR_UNKNOWN"
+    assert lib.zoomr_abi_version() == 1
+
+
+def test_host_argument_errors_without_a_device(lib):
+    from paper_2604_10898_b200 import zoomr as Z
+    g = Z.Geom(32, 32, 8, 128, 64)
+    # NULL pointers -> ZOOMR_ERR_INVALID_ARG, nothing enqueued
+    assert lib.zoomr_score(C.byref(g), 1, None, None, None, 16, 2, None, None, None, None, None) == 1
+    bad = Z.Geom(32, 30, 8, 128, 64)  # H_q % H_kv != 0
+    assert lib.zoomr_score(C.byref(bad), 1, None, None, None, 16, 2, None, None, None, None, None) == 2
+    odd = Z.Geom(32, 32, 8, 96, 64)   # unsupported head_dim
+    assert lib.zoomr_score(C.byref(odd), 1, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), 16, 2,
+                           C.c_void_p(16), None, None, None, None) == 7
+    lib.zoomr_attn_workspace_bytes.restype = C.c_size_t
+    assert lib.zoomr_attn_workspace_bytes(C.byref(bad), 1) == 0
+    assert lib.zoomr_build_index(1, None, None, 4, 0, None, 16, None, None, None) == 1

@@ -56,6 +56,27 @@ inline void prefer_max_smem(F *kfn) {
   if (mode >= 0) cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, mode);
 }
 
+// Launch with programmatic dependent launch (PDL): the kernel may start while
+// its predecessor on the stream is finishing; it must execute
+// `griddepcontrol.wait` before touching the predecessor's outputs.
+template <typename Kern, typename... Args>
+inline void launch_pdl(Kern kfn, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kfn, args...);
+}
+
+// Let the next kernel on the stream (launched with PDL) begin its prologue.
+__device__ __forceinline__ void allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 inline bool valid_geom(const zoomr_geom *g) {
   if (!g) return false;
   if (g->num_layers < 1 || g->num_q_heads < 1 || g->num_kv_heads < 1 || g->page_size < 1) return false;

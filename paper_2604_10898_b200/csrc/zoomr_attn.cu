@@ -39,7 +39,8 @@
 namespace zoomr {
 
 constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addresses)
-constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
+constexpr int kPairs = 4;   // math warps per CTA, each fed by kProd producer warps
+constexpr int kProd = 1;    // producer warps per math warp (2 measured no faster: LDGSTS path caps ~5.5 TB/s)
 constexpr int kStages = 3;  // ring depth per pair
 
 template <int D>
@@ -70,11 +71,15 @@ struct AttnParams {
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
   float scale_log2;
   int32_t *status;
+  int32_t debug_mode;  // 0 normal; 1 math skipped; 2 copies skipped (A/B experiments only)
 };
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16_l2pf(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -152,7 +157,7 @@ struct Sched {
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kernel(const AttnParams p) {
   using S = AttnShape<D>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kPairs][kStages]
@@ -163,11 +168,14 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
 
   if (threadIdx.x == 0) {
     for (int x = 0; x < kPairs * kStages; ++x) {
-      mbar_init(&full[x], 32);  // one cp.async arrive (noinc) per producer lane
+      mbar_init(&full[x], 32 * kProd);  // one cp.async arrive (noinc) per producer lane
       mbar_init(&empty[x], 1);  // the math warp's lane 0
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Programmatic dependent launch: everything above overlaps the producer of
+  // I_f (a4 / the fused select); from here on its results are visible.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // tiles per sequence -> prefix (warp 0 scans in chunks of 32 sequences)
   if (warp == 0) {
     int carry = 0;
@@ -203,6 +211,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
 
   const int pair = warp % kPairs;
   const bool producer = warp >= kPairs;
+  const int psub = producer ? (warp - kPairs) / kPairs : 0;  // which half of each tile this producer copies
   const int64_t gw = (int64_t)blockIdx.x * kPairs + pair;  // global math-warp id of the pair
   if (gw >= sc.NWe) return;
   const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
@@ -212,44 +221,95 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
   uint64_t *emptyp = empty + pair * kStages;
 
   if (producer) {
-    // ================= producer: resolve rows one tile ahead, LDGSTS them ====
-    auto resolve = [&](int64_t k, const __nv_bfloat16 *&krow, const __nv_bfloat16 *&vrow, int &ok) {
-      int b, seg, tis, nts;
-      sc.locate(r0 + k, b, seg, tis, nts);
-      int cnt = p.count[b];
+    // ================= producer: 3-stage address pipeline, LDGSTS copies =====
+    // A(k+2): I_f position load   B(k+1): page-table load   C(k): row copies.
+    // Each dependent load is consumed one iteration after it is issued, so the
+    // index -> page -> row chain never stalls the copy issue in steady state.
+    struct Addr {
+      int b, l, g, ok, tok, slot, page;
+    };
+    auto stage_a = [&](int64_t k, Addr &a) {
+      int seg, tis, nts;
+      sc.locate(r0 + k, a.b, seg, tis, nts);
+      int cnt = p.count[a.b];
       cnt = cnt < p.cap ? cnt : p.cap;
-      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      a.l = seg / p.Hkv;
+      a.g = seg - a.l * p.Hkv;
       const int pos = tis * kTile + lane;
-      ok = pos < cnt;
-      krow = p.kpool;
-      vrow = p.vpool;
-      if (ok) {
-        const int tok = p.index[(int64_t)b * p.cap + pos];
-        const int lp = p.Pshift >= 0 ? (tok >> p.Pshift) : tok / p.P;
-        const int slot = tok - lp * p.P;
-        int page = 0;
-        if (tok >= 0 && lp < p.max_pages) page = p.page_table[(int64_t)b * p.max_pages + lp];
-        if (tok < 0 || lp >= p.max_pages || page < 0 || page >= p.num_pages) {
+      a.ok = pos < cnt;
+      a.tok = a.ok ? p.index[(int64_t)a.b * p.cap + pos] : 0;
+    };
+    auto stage_b = [&](Addr &a) {
+      a.page = 0;
+      a.slot = 0;
+      if (a.ok) {
+        const int lp = p.Pshift >= 0 ? (a.tok >> p.Pshift) : a.tok / p.P;
+        a.slot = a.tok - lp * p.P;
+        if (a.tok >= 0 && lp < p.max_pages) a.page = p.page_table[(int64_t)a.b * p.max_pages + lp];
+        else a.page = -1;
+      }
+    };
+    // pipeline depth: the I_f load runs kAheadA tiles ahead, the page-table load
+    // kAheadB tiles ahead of the copies
+    constexpr int kAheadA = 4, kAheadB = 2;
+    Addr q0{}, q1{}, q2{}, q3{}, q4{};  // tiles k .. k+4
+    if (ntiles > 0) stage_a(0, q0);
+    if (ntiles > 1) stage_a(1, q1);
+    if (ntiles > 2) stage_a(2, q2);
+    if (ntiles > 3) stage_a(3, q3);
+    if (ntiles > 0) stage_b(q0);
+    if (ntiles > 1) stage_b(q1);
+    const int rsub = lane / S::CPR, ch = lane % S::CPR;
+    for (int64_t k = 0; k < ntiles; ++k) {
+      if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
+      if (k + kAheadB < ntiles) stage_b(q2);
+      Addr &ac = q0;
+      // stage C: row addresses of tile k
+      const __nv_bfloat16 *ck = p.kpool, *cv = p.vpool;
+      int cok = ac.ok;
+      if (cok) {
+        int page = ac.page;
+        if (page < 0 || page >= p.num_pages) {
           set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
           page = 0;
         }
-        const int64_t row = (((int64_t)l * p.num_pages + page) * p.Hkv + g) * p.P + slot;
-        krow = p.kpool + row * D;
-        vrow = p.vpool + row * D;
+        const int64_t row = (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot;
+        ck = p.kpool + row * D;
+        cv = p.vpool + row * D;
       }
-    };
-    const __nv_bfloat16 *ck = nullptr, *cv = nullptr, *nk = nullptr, *nv = nullptr;
-    int cok = 0, nok = 0;
-    if (ntiles > 0) resolve(0, ck, cv, cok);
-    const int rsub = lane / S::CPR, ch = lane % S::CPR;
-    for (int64_t k = 0; k < ntiles; ++k) {
-      if (k + 1 < ntiles) resolve(k + 1, nk, nv, nok);  // loads overlap the wait + copies below
       const int s = (int)(k % kStages);
       mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1));
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
       const uint32_t stV = stK + S::TILE_BYTES;
+      if (p.debug_mode == 2) cok = 0;
+      if (p.debug_mode == 16 && S::CPR >= 2) {
+        // variant: each lane copies one whole 32-byte sector (two 16-byte halves)
+        constexpr int LPR = S::CPR / 2, RPI2 = 32 / LPR;
+        const int rs2 = lane / LPR, c2 = lane % LPR;
 #pragma unroll
-      for (int i = 0; i < kTile / S::RPI; ++i) {
+        for (int i = 0; i < kTile / RPI2; ++i) {
+          const int r = i * RPI2 + rs2;
+          const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
+          const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
+          const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;
+          cp_async16(stK + r * S::RS + c2 * 32, kr + c2 * 16, n);
+          cp_async16(stK + r * S::RS + c2 * 32 + 16, kr + c2 * 16 + 8, n);
+          cp_async16(stV + r * S::RS + c2 * 32, vr + c2 * 16, n);
+          cp_async16(stV + r * S::RS + c2 * 32 + 16, vr + c2 * 16 + 8, n);
+        }
+      } else if (p.debug_mode == 32) {
+#pragma unroll
+        for (int i = 0; i < kTile / S::RPI; ++i) {
+          const int r = i * S::RPI + rsub;
+          const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
+          const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
+          const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;
+          cp_async16_l2pf(stK + r * S::RS + ch * 16, kr + ch * 8, n);
+          cp_async16_l2pf(stV + r * S::RS + ch * 16, vr + ch * 8, n);
+        }
+      } else {
+#pragma unroll
+      for (int i = psub; i < kTile / S::RPI; i += kProd) {
         const int r = i * S::RPI + rsub;  // token row of this lane's chunk
         const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
         const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
@@ -257,10 +317,12 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
         cp_async16(stK + r * S::RS + ch * 16, kr + ch * 8, n);
         cp_async16(stV + r * S::RS + ch * 16, vr + ch * 8, n);
       }
+      }
       cp_async_arrive_noinc(&fullp[s]);
-      ck = nk;
-      cv = nv;
-      cok = nok;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      q3 = q4;
     }
     return;
   }
@@ -352,14 +414,14 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
         }
       }
     }
-    __threadfence();
-    __syncwarp();
+    __syncwarp();  // orders the lanes' partial stores before lane 0's release
     int32_t *cnt = p.ws_cnt + (int64_t)b * sc.LH + seg;
     int old = 0;
-    if (lane == 0) old = atomicAdd(cnt, 1);
+    if (lane == 0)
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != (int)(wl - wf)) return;  // not the last arriving warp
-    __threadfence();
+    __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
     // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic)
     const int nparts = (int)(wl - wf + 1);
     float Mh[G], Lh[G];
@@ -459,6 +521,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1) sparse_attn_kernel(const AttnP
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
     const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
     const uint32_t stV = stK + S::TILE_BYTES;
+    if (p.debug_mode == 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyp[s]);
+      continue;
+    }
 
     // ---- S = K . Q^T  (2 m-tiles of 16 tokens) ----
     float sacc[2][4];
@@ -611,6 +678,14 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
   prm.status = dev_status;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char *e = getenv("ZOOMR_ATTN_DEBUG_MODE");
+      dbg = e ? atoi(e) : 0;
+    }
+    prm.debug_mode = dbg;
+  }
   const int G = geom->num_q_heads / geom->num_kv_heads;
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = attn_grid();
@@ -621,7 +696,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                 \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
     prefer_max_smem(kfn);                                                                \
-    kfn<<<grid, 64 * kPairs, smem, s>>>(prm);                                            \
+    launch_pdl(kfn, grid, 32 * kPairs * (1 + kProd), smem, s, prm);                      \
   } while (0)
 #define ZOOMR_AT_G(DD)               \
   switch (G) {                       \

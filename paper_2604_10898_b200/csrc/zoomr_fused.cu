@@ -62,6 +62,7 @@ template <int D, int G>
 __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
+  allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
   const int lg = blockIdx.x, b = blockIdx.y;
   const int l = lg / p.Hkv, g = lg - l * p.Hkv;
   const int Hq = p.Hkv * G, V = p.L * Hq, MS = p.max_summaries;

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(512) build_index_kernel(
     int32_t *__restrict__ index_count, int32_t *status) {
   extern __shared__ int32_t off[];  // [2*max_summaries] clipped pieces: start, offset
   __shared__ int32_t scratch[40];
+  allow_dependents();
   const int b = blockIdx.x;
   const int T = seq_len[b];
   int nt = num_summaries[b];

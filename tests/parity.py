@@ -178,3 +178,91 @@ def run_full(inp, step, fused=False):
     step.run(inp.q, kv, seg, close_items=close, fused=fused)
     torch.cuda.synchronize()
     step.check_status()
+
+
+def gather_tokens(inp, b, positions, which="k", layers=None, heads=None):
+    """Rows of sequence b at the given absolute token positions: uint16 [n][L'][H'][d] (host).
+
+    Plumbing only (page-table gather with torch indexing on the device, then a
+    host copy of just those rows) so that full-size configs can be checked on
+    sampled outputs without copying the whole cache."""
+    cfg = inp.cfg
+    pool = inp.k_pool if which == "k" else inp.v_pool
+    dev = pool.device
+    pos = torch.as_tensor(np.asarray(positions, dtype=np.int64), device=dev)
+    pt = inp.page_table[b].long()
+    pages = pt[pos // cfg.page]
+    slots = pos % cfg.page
+    lay = torch.arange(cfg.L, device=dev) if layers is None else torch.as_tensor(list(layers), device=dev)
+    hed = torch.arange(cfg.Hkv, device=dev) if heads is None else torch.as_tensor(list(heads), device=dev)
+    sub = pool.index_select(0, lay)                      # [L'][pages][Hkv][P][d]
+    rows = sub[:, pages, :, slots]     # advanced indices separated by a slice go first: [n][L'][Hkv][d]
+    rows = rows.index_select(2, hed)   # [n][L'][H'][d]
+    return bf16_bits(rows.contiguous())
+
+
+def check_sequence_sampled(inp, step, b, report, layers, qheads):
+    """Full-size parity on sampled outputs: selection over ALL voters (votes are a
+    global aggregate), mean keys / alpha checked on every layer, attention on the
+    sampled (layer, query head) pairs only."""
+    cfg = inp.cfg
+    L, Hq, Hkv, d = cfg.L, cfg.Hq, cfg.Hkv, cfg.d
+    G = Hq // Hkv
+    seg = seg_host(inp, b)
+    n = len(seg)
+    T = int(inp.seq_len[b])
+    q = bf16_bits(inp.q[b])
+    # summary tokens only, compacted (mean keys read nothing else)
+    spos = np.concatenate([np.arange(s[2], s[3]) for s in seg])
+    Ks = gather_tokens(inp, b, spos, "k")
+    cseg, off = [], 0
+    for s in seg:
+        ln = s[3] - s[2]
+        cseg.append([off, off, off, off + ln])
+        off += ln
+    mk_ref = oracle.update_mean_keys(Ks, np.array(cseg, np.int32), L, Hkv, d)
+    mk_gpu = step.mean_keys[b, :, :, :n].cpu().numpy()
+    assert np.array_equal(mk_gpu, mk_ref.astype(np.float32)), "a1 mean keys differ"
+    sc = oracle.score(q, mk_ref, cfg.top_k, L, Hq, Hkv, d)
+    al_gpu = step.alpha[b, :, :, :n].cpu().numpy().astype(np.float64)
+    M = alpha_scale(q, mk_ref)
+    err = np.abs(al_gpu - sc["alpha"]) / np.maximum(M, 1e-30)
+    report["alpha_max_rel_err"] = max(report.get("alpha_max_rel_err", 0.0), float(err.max()))
+    assert err.max() <= ALPHA_TOL
+    topk_gpu = step.topk[b].cpu().numpy()
+    kk = min(cfg.top_k, n)
+    al_ref = sc["alpha"].reshape(L * Hq, n)
+    for v in range(L * Hq):
+        g_set, r_set = topk_gpu[v, :kk].tolist(), sc["topk"][v].tolist()
+        if set(g_set) != set(r_set):
+            assert set_ok_modulo_near_ties(g_set, r_set, al_ref[v]), f"voter {v}"
+            report["excused_voters"] = report.get("excused_voters", 0) + 1
+    votes_ref, A_ref = oracle.aggregate(sc["alpha"], topk_gpu[:, :kk].copy(), L, Hq, Hkv, d)
+    part = step.partial[b, :, :n].cpu().numpy()
+    assert np.array_equal(part[0], votes_ref), "votes differ"
+    A_gpu = part[1].astype(np.float64) / 2.0 ** 32
+    flags_gpu = step.flags[b, :n].cpu().numpy()
+    flags_same_in, _, _ = oracle.select_topc(part[0], A_gpu, cfg.c)
+    assert np.array_equal(flags_gpu, flags_same_in)
+    flags_ref, _, _ = oracle.select_topc(votes_ref, A_ref, cfg.c)
+    if not np.array_equal(flags_gpu, flags_ref):
+        zc_g, zc_r = set(np.nonzero(flags_gpu == 2)[0]), set(np.nonzero(flags_ref == 2)[0])
+        assert all(votes_ref[i] == votes_ref[j] and near(A_ref[i], A_ref[j]) for i in zc_r - zc_g for j in zc_g - zc_r)
+        report["excused_cuts"] = report.get("excused_cuts", 0) + 1
+    idx_ref = oracle.build_index(seg, flags_gpu, T, step.params.sink, step.params.window)
+    cnt = int(step.count[b])
+    assert cnt == len(idx_ref) and np.array_equal(step.index[b, :cnt].cpu().numpy(), idx_ref)
+    report.setdefault("index_counts", []).append(cnt)
+    out_gpu = step.out[b].cpu().numpy().astype(np.float64)
+    kvheads = sorted({h // G for h in qheads})
+    for l in layers:
+        Kr = gather_tokens(inp, b, idx_ref, "k", layers=[l], heads=kvheads)
+        Vr = gather_tokens(inp, b, idx_ref, "v", layers=[l], heads=kvheads)
+        for h in qheads:
+            j = kvheads.index(h // G)
+            o = oracle.attend_one(q[l, h], np.ascontiguousarray(Kr[:, 0, j]), np.ascontiguousarray(Vr[:, 0, j]),
+                                  np.arange(len(idx_ref)))
+            e = float(np.abs(out_gpu[l, h] - o).max())
+            report["attn_max_abs_err"] = max(report.get("attn_max_abs_err", 0.0), e)
+            assert e <= ATTN_TOL
+    return report

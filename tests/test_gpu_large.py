@@ -1,0 +1,101 @@
+"""Full-size GPU parity (BASELINE configs[1..3]) on sampled outputs, and the
+KV-head-sharded exchange simulated on one GPU (one a2 per head shard, partials
+summed in rank order) -- NCCL refuses several ranks on one GPU, so the real
+all-reduce runs only on a multi-GPU box; the CPU gloo tests cover its host path."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import zoomr_synth as S
+from tests import parity as PY
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    oracle.build()
+    from paper_2604_10898_b200 import _build
+    _build.build()
+
+
+def _run(inp, fused=True, capacity=None):
+    st = PY.make_step(inp, capacity=capacity)
+    PY.run_full(inp, st, fused=fused)
+    return st
+
+
+def test_70b64k_full_size_sampled():
+    inp = S.generate(S.CONFIGS["70b64k"], device="cuda")
+    st = _run(inp, capacity=16384)
+    rep = PY.check_sequence_sampled(inp, st, 0, {}, layers=[0, 41, 79], qheads=[0, 9, 63])
+    print(rep)
+    del st, inp
+    torch.cuda.empty_cache()
+
+
+def test_8b32k_batch_subset():
+    cfg = dataclasses.replace(S.CONFIGS["8b32k"], batch=3)
+    inp = S.generate(cfg, device="cuda")
+    st = _run(inp, capacity=8192)
+    rep = {}
+    for b in range(3):
+        PY.check_sequence_sampled(inp, st, b, rep, layers=[0, 31], qheads=[0, 31])
+    print(rep)
+
+
+def test_8b32k_jitter_layout():
+    cfg = dataclasses.replace(S.CONFIGS["8b32k"], batch=2, jitter=True)
+    inp = S.generate(cfg, device="cuda")
+    st = _run(inp, capacity=8192, fused=False)
+    rep = {}
+    for b in range(2):
+        PY.check_sequence_sampled(inp, st, b, rep, layers=[5], qheads=[3, 17])
+
+
+@pytest.mark.parametrize("cfg_name,world", [("8b16k", 8), ("8b16k", 2), ("tiny", 2)])
+def test_head_sharded_exchange_simulated(cfg_name, world):
+    """a2 per KV-head shard + sum of int64 partials == unsharded a2, bit for bit;
+    hence identical flags / I_f on every rank, and per-shard a5 == unsharded a5."""
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.parallel import HeadShardedStep, local_shape, shard_heads, slice_heads
+    from paper_2604_10898_b200.step import StepParams, ZoomrStep
+    cfg = S.CONFIGS[cfg_name]
+    inp = S.generate(cfg, device="cuda")
+    full = PY.make_step(inp, capacity=cfg.T)
+    PY.run_full(inp, full, fused=False)
+    torch.cuda.synchronize()
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    prm = StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    steps, parts = [], []
+    for r in range(world):
+        sh = shard_heads(cfg.Hq, cfg.Hkv, r, world)
+        kp, vp, qq = slice_heads(inp.k_pool, inp.v_pool, inp.q, sh)
+        st = ZoomrStep(local_shape(shape, sh), 1, inp.bounds.shape[1], cfg.T, prm)
+        kv = (kp, vp, inp.page_table)
+        st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+        Z.score(st.shape, qq, st.mean_keys, inp.num_summaries, cfg.top_k, st.partial, dev_status=st.status)
+        steps.append((st, kv, qq, sh))
+        parts.append(st.partial.clone())
+    total = torch.zeros_like(parts[0])
+    for p in parts:  # the all-reduce(SUM), in rank order
+        total += p
+    assert torch.equal(total, full.partial)
+    for st, kv, qq, sh in steps:  # every rank: a3, a4 on identical inputs, then local a5
+        st.partial.copy_(total)
+        Z.select_topc(st.partial, inp.num_summaries, cfg.c, st.flags, st.agreeability, st.status)
+        Z.build_index(inp.bounds, inp.num_summaries, inp.seq_len, st.flags, cfg.sink, cfg.window, st.index, st.count,
+                      st.status)
+        Z.sparse_decode_attn(st.shape, qq, kv[0], kv[1], kv[2], st.index, st.count, st.out, st.workspace,
+                             dev_status=st.status)
+        torch.cuda.synchronize()
+        st.check_status()
+        assert torch.equal(st.flags, full.flags) and torch.equal(st.count, full.count)
+        assert torch.equal(st.index, full.index)
+        torch.testing.assert_close(st.out, full.out[:, :, sh.q_start:sh.q_stop], atol=2e-6, rtol=0)

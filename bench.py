@@ -174,9 +174,15 @@ def oracle_time(inp, seconds, threads=0):
 
 
 def run_reference(args):
+    """Reference arm = the CPU oracle (there is no reference implementation to
+    install: /root/reference holds only the paper and a spec).  Each timed step is
+    a bounded sample of the workload: the full selection (a1-a4 over all layers
+    and voters) plus attention for a rotating 1/8 of the layers; the reported
+    seqs/s extrapolates the sampled attention to all layers."""
     rank, world, local = init_dist(args.gpus)
     if rank != 0:
         return
+    import numpy as np
     import zoomr_synth as S
     cfg = S.CONFIGS[args.workload]
     dev = "cuda" if torch.cuda.is_available() else "cpu"
@@ -189,28 +195,46 @@ def run_reference(args):
     q = bf16_bits(inp.q[0])
     n = int(inp.num_summaries[0])
     seg = inp.bounds[0, :n].cpu().numpy()
+    T = K.shape[0]
+    frac = 8
+    per = max(1, cfg.L // frac)
+    t_sel = t_att = 0.0
+    count = 0
 
-    def one():
-        return oracle.step(q, K, V, seg, cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.top_k, cfg.c, cfg.sink,
-                           cfg.window)
-    for _ in range(args.warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        r = one()
-    el = time.perf_counter() - t0
-    val = args.steps * inp.q.shape[0] / el
+    def one(i):
+        nonlocal t_sel, t_att, count
+        t0 = time.perf_counter()
+        mk = oracle.update_mean_keys(K, seg, cfg.L, cfg.Hkv, cfg.d)
+        sc = oracle.score(q, mk, cfg.top_k, cfg.L, cfg.Hq, cfg.Hkv, cfg.d)
+        flags, _, _ = oracle.select_topc(sc["votes"], sc["A"], cfg.c)
+        idx = oracle.build_index(seg, flags, T, cfg.sink, cfg.window)
+        t1 = time.perf_counter()
+        l0 = (i * per) % cfg.L
+        ls = slice(l0, l0 + per)
+        oracle.sparse_decode_attn(np.ascontiguousarray(q[ls]), np.ascontiguousarray(K[:, ls]),
+                                  np.ascontiguousarray(V[:, ls]), idx, per, cfg.Hq, cfg.Hkv, cfg.d)
+        t2 = time.perf_counter()
+        count = len(idx)
+        return t1 - t0, t2 - t1
+    for i in range(args.warmup):
+        one(i)
+    for i in range(args.steps):
+        a, b = one(i)
+        t_sel += a
+        t_att += b
+    step_s = (t_sel + t_att * cfg.L / per) / args.steps
+    val = inp.q.shape[0] / step_s
     cores = oracle.num_threads(0)
+    sample = (f"per step: full a1-a4 selection over all {cfg.L}x{cfg.Hq} voters + a5 attention for {per} of "
+              f"{cfg.L} layers (rotating), extrapolated to all layers; one {cfg.name} sequence")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "seqs/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg.name, "batch": inp.q.shape[0], "T": cfg.T, "n_summaries": n,
-                   "index_count": int(len(r["index"])), "query": args.query},
-        "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle",
-                         "sample": f"full oracle step (a1-a5, all {cfg.L}x{cfg.Hq} heads) of one "
-                                   f"{cfg.name} sequence per step"},
+                   "index_count": int(count), "query": args.query},
+        "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

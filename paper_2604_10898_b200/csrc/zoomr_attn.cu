@@ -11,19 +11,20 @@
 //    balance whatever |I_f| turns out to be on the device, and at most two
 //    partial results per warp.  Segments split across warps are merged by the
 //    last-arriving warp (arrival counter per segment, self-resetting).
-//  * Warp specialisation in producer/consumer PAIRS.  The gather address chain
-//    (I_f position -> page table -> row address: two dependent L2 loads) is
-//    decoupled from the math: producer warp p resolves tile k+1 while it copies
-//    tile k for math warp p, with 16-byte cp.async.cg (LDGSTS, L1 bypass; one
-//    warp instruction moves whole 256-byte rows, 16 lanes per row) into a
-//    kStages-deep ring of shared-memory tiles whose rows are padded to a
-//    2*d+16 byte stride (conflict-free ldmatrix).  Completion is signalled with
-//    cp.async.mbarrier.arrive.noinc on a per-stage mbarrier; the math warp frees
-//    the stage with a plain mbarrier arrive.  Rows past the end of a segment are
-//    zero-filled by the copy (src-size 0).  (Version 0 issued one TMA bulk copy
-//    per 256-byte row: ncu showed the producer issue-bound at ~90 cycles per
-//    copy -- profiles/r01_k5_v0_*; version 1 did gather and math in the same
-//    warp and was latency-bound -- profiles/r01_k5_v1_*.)
+//  * Warp specialisation in producer/consumer PAIRS.  The producer warp runs a
+//    5-deep address pipeline (I_f position 4 tiles ahead, page-table entry 2
+//    tiles ahead) and gathers each 32-token K/V tile with TMA: the tile's
+//    tokens are cut into runs of consecutive tokens in one page, each run into
+//    16- and 8-row boxes loaded by cp.async.bulk.tensor (2D tensor map over the
+//    whole pool, 128-byte swizzle: rows land bank-conflict-free for ldmatrix),
+//    and the < 8-row leftovers (plus zero-filled rows past the end of a
+//    segment) by 16-byte cp.async with the same swizzle applied by hand.  TMA
+//    bytes complete on the stage's mbarrier (expect_tx), the cp.async part via
+//    cp.async.mbarrier.arrive.noinc on the same barrier; the math warp frees the
+//    stage with a plain arrive.  History (profiles/): v0 one TMA bulk copy per
+//    256-byte row (issue-bound, 12 % of peak); v1 gather + math in one warp
+//    (latency-bound, 27 %); v2/v3 LDGSTS producer (72 %, capped by the LDGSTS
+//    path: tools/bench_gather.cu measures <= 5.3 TB/s); v4 this TMA gather.
 //  * Math on tensor cores (mma.sync m16n8k16, bf16 in, fp32 accumulate):
 //      S^T-tile = K_tile (32 tok x d) . Q^T (d x 8 padded heads)
 //      O^T     += V_tile^T (d x 32 tok) . P (32 tok x 8)
@@ -34,25 +35,41 @@
 //    SURVEY 7.3-1) at no extra MMA for G <= 4.  The S accumulator fragment is
 //    transposed into the PV B-operand with movmatrix.
 //  * fp32 online softmax (exp2 with scale*log2e folded in), fp32 output.
+#include <cuda.h>  // CUtensorMap (the encode entry point is fetched through the runtime)
+
 #include "common.cuh"
 
 namespace zoomr {
 
 constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addresses)
-constexpr int kPairs = 4;   // math warps per CTA, each fed by kProd producer warps
-constexpr int kProd = 1;    // producer warps per math warp (2 measured no faster: LDGSTS path caps ~5.5 TB/s)
+constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
 constexpr int kStages = 3;  // ring depth per pair
 
 template <int D>
 struct AttnShape {
-  static constexpr int RB = 2 * D;               // bytes of one K or V row (bf16)
-  static constexpr int RS = 2 * D + 16;          // padded smem row stride (conflict-free ldmatrix)
-  static constexpr int CPR = RB / 16;            // 16-byte chunks per row
-  static constexpr int RPI = 32 / CPR;           // rows copied per warp instruction
-  static constexpr int TILE_BYTES = kTile * RS;  // K (or V) part of a stage
+  static constexpr int RB = 2 * D;                      // bytes of one K or V row (bf16)
+  static constexpr bool SWZ = D >= 64;                  // 128-byte swizzled 64-column regions
+  static constexpr int NREG = SWZ ? D / 64 : 1;         // regions per tile (column halves)
+  static constexpr int RBR = SWZ ? 128 : RB;            // bytes of a row inside one region
+  static constexpr int BX = SWZ ? 64 : D;               // TMA box inner extent (elements)
+  static constexpr int REG_BYTES = kTile * RBR;         // one region of one tile
+  static constexpr int TILE_BYTES = NREG * REG_BYTES;   // K (or V) part of a stage
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
   static constexpr int RING_BYTES = kPairs * kStages * STAGE_BYTES;
   static constexpr int BAR_BYTES = 2 * kPairs * kStages * 8;
+  static constexpr int CPR = RB / 16;                   // 16-byte chunks per row
+  static constexpr int RPI = 32 / CPR;                  // rows per warp-wide cp.async
+  // shared address of (row r, 16-byte chunk c) inside a K or V tile starting at `base`
+  __device__ static __forceinline__ uint32_t at(uint32_t base, int r, int c) {
+    if constexpr (SWZ)
+      return base + (uint32_t)((c >> 3) * REG_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+    else
+      return base + (uint32_t)(r * RB + (c << 4));
+  }
+};
+
+struct TmaMaps {
+  CUtensorMap k16, k8, v16, v8;  // 2D [total rows][D] views of the pools, boxes of 16 / 8 rows
 };
 
 struct AttnParams {
@@ -71,21 +88,26 @@ struct AttnParams {
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
   float scale_log2;
   int32_t *status;
-  int32_t debug_mode;  // 0 normal; 1 math skipped; 2 copies skipped (A/B experiments only)
 };
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async16_l2pf(uint32_t dst, const void *src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int64_t y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(x), "r"((int)y), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -157,9 +179,12 @@ struct Sched {
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(64 * kPairs, 1)
+    sparse_attn_kernel(const AttnParams p, const __grid_constant__ TmaMaps maps) {
   using S = AttnShape<D>;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  // the 128-byte swizzle pattern follows address bits [7:9]: keep the ring 1024-aligned
+  unsigned char *smem = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kPairs][kStages]
   uint64_t *empty = full + kPairs * kStages;                             // [kPairs][kStages]
   int32_t *prefix = reinterpret_cast<int32_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // [B+1]
@@ -168,7 +193,7 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
 
   if (threadIdx.x == 0) {
     for (int x = 0; x < kPairs * kStages; ++x) {
-      mbar_init(&full[x], 32 * kProd);  // one cp.async arrive (noinc) per producer lane
+      mbar_init(&full[x], 33);  // producer lane 0's expect_tx arrive + one cp.async (noinc) arrive per lane
       mbar_init(&empty[x], 1);  // the math warp's lane 0
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -211,7 +236,6 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
 
   const int pair = warp % kPairs;
   const bool producer = warp >= kPairs;
-  const int psub = producer ? (warp - kPairs) / kPairs : 0;  // which half of each tile this producer copies
   const int64_t gw = (int64_t)blockIdx.x * kPairs + pair;  // global math-warp id of the pair
   if (gw >= sc.NWe) return;
   const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
@@ -264,59 +288,73 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
       if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
       if (k + kAheadB < ntiles) stage_b(q2);
       Addr &ac = q0;
-      // stage C: row addresses of tile k
-      const __nv_bfloat16 *ck = p.kpool, *cv = p.vpool;
-      int cok = ac.ok;
-      if (cok) {
-        int page = ac.page;
-        if (page < 0 || page >= p.num_pages) {
-          set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
-          page = 0;
-        }
-        const int64_t row = (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot;
-        ck = p.kpool + row * D;
-        cv = p.vpool + row * D;
+      // stage C: global row of every token of tile k
+      const int cok = ac.ok;
+      int page = ac.page;
+      if (cok && (page < 0 || page >= p.num_pages)) {
+        set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+        page = 0;
       }
+      const int64_t grow = cok ? (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot : 0;
+      // runs of consecutive tokens in one page -> boxes of 16 / 8 rows; the rest by cp.async
+      const int ptok = __shfl_up_sync(0xffffffffu, ac.tok, 1);
+      const int ppage = __shfl_up_sync(0xffffffffu, page, 1);
+      const int pok = __shfl_up_sync(0xffffffffu, cok, 1);
+      const bool cont = cok && lane > 0 && pok && ptok + 1 == ac.tok && ppage == page;
+      const unsigned validm = __ballot_sync(0xffffffffu, cok);
+      const unsigned startm = __ballot_sync(0xffffffffu, cok && !cont);
+      const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+      const int rs = 31 - __clz(startm & upto | 1u);               // my run's first slot
+      const unsigned after = (startm | ~validm) & ~upto;
+      const int re = after ? __ffs(after) - 1 : 32;                // one past my run's last slot
+      const int pos = lane - rs, len = re - rs;
+      const int n16 = (len >> 4) << 4, n8 = ((len & 15) >> 3) << 3;
+      // TMA boxes need 128-byte aligned destinations: d >= 64 only (d < 64 configs are toy-sized)
+      const bool lead16 = S::SWZ && cok && pos < n16 && (pos & 15) == 0;
+      const bool lead8 = S::SWZ && cok && n8 && pos == n16;
+      const bool byhand = !cok || !S::SWZ || pos >= n16 + n8;
+      const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8);
+      const uint32_t tx = (uint32_t)((__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
       const int s = (int)(k % kStages);
       mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1));
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
       const uint32_t stV = stK + S::TILE_BYTES;
-      if (p.debug_mode == 2) cok = 0;
-      if (p.debug_mode == 16 && S::CPR >= 2) {
-        // variant: each lane copies one whole 32-byte sector (two 16-byte halves)
-        constexpr int LPR = S::CPR / 2, RPI2 = 32 / LPR;
-        const int rs2 = lane / LPR, c2 = lane % LPR;
+      if (lane == 0) mbar_arrive_expect_tx(&fullp[s], tx);
+      __syncwarp();
+      if (lead16 || lead8) {
+        const CUtensorMap *mk = lead16 ? &maps.k16 : &maps.k8;
+        const CUtensorMap *mv = lead16 ? &maps.v16 : &maps.v8;
 #pragma unroll
-        for (int i = 0; i < kTile / RPI2; ++i) {
-          const int r = i * RPI2 + rs2;
-          const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
-          const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
-          const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;
-          cp_async16(stK + r * S::RS + c2 * 32, kr + c2 * 16, n);
-          cp_async16(stK + r * S::RS + c2 * 32 + 16, kr + c2 * 16 + 8, n);
-          cp_async16(stV + r * S::RS + c2 * 32, vr + c2 * 16, n);
-          cp_async16(stV + r * S::RS + c2 * 32 + 16, vr + c2 * 16 + 8, n);
+        for (int rg = 0; rg < S::NREG; ++rg) {
+          // destination = the row's unswizzled start; the TMA unit applies the 128-byte swizzle
+          const uint32_t off = (uint32_t)(rg * S::REG_BYTES + lane * S::RBR);
+          tma_load_2d(stK + off, mk, rg * S::BX, grow, &fullp[s]);
+          tma_load_2d(stV + off, mv, rg * S::BX, grow, &fullp[s]);
         }
-      } else if (p.debug_mode == 32) {
-#pragma unroll
-        for (int i = 0; i < kTile / S::RPI; ++i) {
-          const int r = i * S::RPI + rsub;
-          const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
-          const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
-          const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;
-          cp_async16_l2pf(stK + r * S::RS + ch * 16, kr + ch * 8, n);
-          cp_async16_l2pf(stV + r * S::RS + ch * 16, vr + ch * 8, n);
-        }
-      } else {
-#pragma unroll
-      for (int i = psub; i < kTile / S::RPI; i += kProd) {
-        const int r = i * S::RPI + rsub;  // token row of this lane's chunk
-        const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)ck, r);
-        const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)cv, r);
-        const uint32_t n = __shfl_sync(0xffffffffu, cok, r) ? 16u : 0u;  // 0: zero-fill past the end
-        cp_async16(stK + r * S::RS + ch * 16, kr + ch * 8, n);
-        cp_async16(stV + r * S::RS + ch * 16, vr + ch * 8, n);
       }
+      // leftover rows (and zero rows past the end): 16-byte cp.async, swizzle by hand
+      unsigned mh = __ballot_sync(0xffffffffu, byhand);
+      const __nv_bfloat16 *krow = p.kpool + grow * D, *vrow = p.vpool + grow * D;
+      const int rsub = lane / S::CPR, ch = lane % S::CPR;
+      while (mh) {
+        int r = -1;
+        unsigned take = mh;
+#pragma unroll
+        for (int u = 0; u < S::RPI; ++u) {  // the u-th pending row goes to lanes [u*CPR, (u+1)*CPR)
+          const int rr = take ? __ffs(take) - 1 : -1;
+          if (u == rsub) r = rr;
+          if (take) take &= take - 1;
+        }
+        mh = take;
+        const int rsrc = r < 0 ? 0 : r;
+        const __nv_bfloat16 *kr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)krow, rsrc);
+        const __nv_bfloat16 *vr = (const __nv_bfloat16 *)__shfl_sync(0xffffffffu, (unsigned long long)vrow, rsrc);
+        const int rok = __shfl_sync(0xffffffffu, cok, rsrc);
+        if (r >= 0) {
+          const uint32_t n = rok ? 16u : 0u;  // 0: zero-fill
+          cp_async16(S::at(stK, r, ch), kr + ch * 8, n);
+          cp_async16(S::at(stV, r, ch), vr + ch * 8, n);
+        }
       }
       cp_async_arrive_noinc(&fullp[s]);
       q0 = q1;
@@ -521,11 +559,6 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
     const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
     const uint32_t stV = stK + S::TILE_BYTES;
-    if (p.debug_mode == 1) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyp[s]);
-      continue;
-    }
 
     // ---- S = K . Q^T  (2 m-tiles of 16 tokens) ----
     float sacc[2][4];
@@ -537,7 +570,7 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
       for (int ks = 0; ks < NKS; ++ks) {
         uint32_t a0, a1, a2, a3;
         const int row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        ldsm_x4(stK + row * S::RS + (ks * 2 + (lane >> 4)) * 16, a0, a1, a2, a3);
+        ldsm_x4(S::at(stK, row, ks * 2 + (lane >> 4)), a0, a1, a2, a3);
         mma_bf16(sacc[mt], a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
       }
     }
@@ -608,7 +641,7 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
       for (int kt = 0; kt < 2; ++kt) {
         uint32_t a0, a1, a2, a3;
         const int row = kt * 16 + (lane & 7) + ((lane >> 4) & 1) * 8;
-        ldsm_x4_t(stV + row * S::RS + (me * 2 + ((lane >> 3) & 1)) * 16, a0, a1, a2, a3);
+        ldsm_x4_t(S::at(stV, row, me * 2 + ((lane >> 3) & 1)), a0, a1, a2, a3);
         mma_bf16(o[me], a0, a1, a2, a3, bh[kt][0], bh[kt][1]);
         if constexpr (kTwoN) mma_bf16(o2[me], a0, a1, a2, a3, bl[kt][0], bl[kt][1]);
       }
@@ -621,10 +654,35 @@ __global__ void __launch_bounds__(32 * kPairs * (1 + kProd), 1) sparse_attn_kern
 
 template <int D, int G>
 size_t attn_smem_bytes(int B) {
-  return (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)(B + 1) * sizeof(int32_t);
+  return 1024 + (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)(B + 1) * sizeof(int32_t);
 }
 
 inline int attn_grid() { return num_sms(); }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2D tensor map over a whole pool viewed as [rows][d] bf16, boxes of `box_rows`
+// rows x (64 or d) columns, 128-byte swizzle for d >= 64.
+inline int encode_pool_map(CUtensorMap *m, const void *base, int d, uint64_t rows, int box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return 1;
+  }
+  const bool swz = d >= 64;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {(cuuint32_t)(swz ? 64 : d), (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1;
+}
 
 inline size_t attn_ws_part_floats(const zoomr_geom *g) {
   const int G = g->num_q_heads / g->num_kv_heads;
@@ -678,17 +736,18 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
   prm.status = dev_status;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char *e = getenv("ZOOMR_ATTN_DEBUG_MODE");
-      dbg = e ? atoi(e) : 0;
-    }
-    prm.debug_mode = dbg;
-  }
   const int G = geom->num_q_heads / geom->num_kv_heads;
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = attn_grid();
+  TmaMaps maps;
+  {
+    const uint64_t rows = (uint64_t)geom->num_layers * kv->num_pages * geom->num_kv_heads * geom->page_size;
+    if (rows >= (1ull << 31)) return ZOOMR_ERR_UNSUPPORTED;  // TMA row coordinate is int32
+    const int d = geom->head_dim;
+    if (encode_pool_map(&maps.k16, kv->k, d, rows, 16) || encode_pool_map(&maps.k8, kv->k, d, rows, 8) ||
+        encode_pool_map(&maps.v16, kv->v, d, rows, 16) || encode_pool_map(&maps.v8, kv->v, d, rows, 8))
+      return ZOOMR_ERR_CUDA;
+  }
 #define ZOOMR_AT(DD, GG)                                                                 \
   do {                                                                                   \
     auto kfn = sparse_attn_kernel<DD, GG>;                                               \
@@ -696,7 +755,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                 \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
     prefer_max_smem(kfn);                                                                \
-    launch_pdl(kfn, grid, 32 * kPairs * (1 + kProd), smem, s, prm);                      \
+    launch_pdl(kfn, grid, 64 * kPairs, smem, s, prm, maps);                              \
   } while (0)
 #define ZOOMR_AT_G(DD)               \
   switch (G) {                       \

@@ -270,7 +270,7 @@ def run_ours(args):
         ga = torch.cuda.CUDAGraph()
         with torch.cuda.graph(ga):
             Z.sparse_decode_attn(shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, st.index, st.count,
-                                 st.out, st.workspace, dev_status=st.status)
+                                 st.out, st.workspace, dev_status=st.status, index_phys=st.index_phys)
         sets.append(dict(inp=inp, st=st, g=g, ga=ga, kv=kv, seg=seg, newest=newest))
     torch.cuda.synchronize()
     for s in sets:
@@ -340,7 +340,8 @@ def run_ours(args):
         "a1_a4_fused_select": cap(lambda: Z.select_fused(
             shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, inp.bounds, inp.num_summaries, inp.seq_len,
             s0["newest"], st.mean_keys, cfg.top_k, cfg.c, cfg.sink, cfg.window, st.flags, st.index, st.count,
-            st.sel_workspace, partial=st.partial, agreeability=st.agreeability, dev_status=st.status)),
+            st.sel_workspace, partial=st.partial, agreeability=st.agreeability, dev_status=st.status,
+            index_phys=st.index_phys)),
         "a1_mean_keys": cap(lambda: st.update_mean_keys(s0["kv"], s0["seg"], s0["newest"])),
         "a2_score": cap(lambda: Z.score(shape, inp.q, st.mean_keys, inp.num_summaries, cfg.top_k, st.partial,
                                         dev_status=st.status)),

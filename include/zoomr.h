@@ -163,9 +163,12 @@ size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
  *   out[b,l,h] = sum_{j in I_f,b} softmax_j(q[b,l,h] . k_j * softmax_scale) v_j
  * with k_j, v_j of KV head h/G gathered from the paged pool.  fp32 logits,
  * online softmax and accumulation; out fp32 [B][L][H_q][d].  index / index_count
- * as written by a4 (count >= 1).  softmax_scale is normally 1/sqrt(d). */
+ * as written by a4 (count >= 1).  index_phys (nullable, [B][index_capacity]):
+ * the page-resolved rows zoomr_select_fused can write alongside I_f
+ * (page_table[t/P]*H_kv*P + t%P); when given, the page table is not read.
+ * softmax_scale is normally 1/sqrt(d). */
 int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
-                             const zoomr_kv *kv, const int32_t *index,
+                             const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                              const int32_t *index_count, int32_t index_capacity,
                              float softmax_scale, float *out, void *workspace,
                              size_t workspace_bytes, int32_t *dev_status, void *stream);
@@ -175,7 +178,8 @@ int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *
  * outputs as calling, in order,
  *   zoomr_update_mean_keys(close_items) ; zoomr_score ; zoomr_select_topc ;
  *   zoomr_build_index
- * with the same arguments: each (layer, KV head) CTA recomputes the mean keys
+ * with the same arguments (plus, if index_phys is non-NULL, the page-resolved
+ * row of every I_f entry for zoomr_sparse_decode_attn): each (layer, KV head) CTA recomputes the mean keys
  * of the summaries in close_items (device int32 [n_close][2] of (b, i); may be
  * empty) for its own (l, g), scores, and publishes its voters' top-k; the last
  * CTA of each sequence aggregates (exact integer votes and fixed-point A),
@@ -191,7 +195,7 @@ int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, con
                        const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
                        float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
                        int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
-                       int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                       int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
                        int32_t *topk_out, void *workspace, size_t workspace_bytes,
                        int32_t *dev_status, void *stream);
 

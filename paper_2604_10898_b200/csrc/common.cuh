@@ -51,7 +51,7 @@ inline void prefer_max_smem(F *kfn) {
   static int mode = -2;
   if (mode == -2) {
     const char *e = getenv("ZOOMR_CARVEOUT");
-    mode = e ? atoi(e) : 100;
+    mode = e ? atoi(e) : -1;  // default: leave the carveout to the driver (measured best)
   }
   if (mode >= 0) cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, mode);
 }

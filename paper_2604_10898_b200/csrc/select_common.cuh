@@ -82,7 +82,7 @@ template <int D>
 __device__ void block_mean_key(const __nv_bfloat16 *__restrict__ kpool, int64_t num_pages,
                                const int32_t *__restrict__ pt, int32_t max_pages, int P, int Hkv, int l,
                                int g, int s0, int s1, double *red /* smem [nwarps][D] */,
-                               float *__restrict__ out, int32_t *status) {
+                               float *__restrict__ out, int32_t *status, float *fresh = nullptr) {
   constexpr int EPL = D >= 32 ? D / 32 : 1;
   constexpr int LANES = D >= 32 ? 32 : D;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -120,6 +120,7 @@ __device__ void block_mean_key(const __nv_bfloat16 *__restrict__ kpool, int64_t 
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += red[w * D + e];
     out[e] = (float)(s / (double)(s1 - s0));  // (1/|S_i|) * sum
+    if (fresh) fresh[e] = out[e];
   }
   __syncthreads();
 }
@@ -217,6 +218,112 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
     }
   }
   __syncthreads();
+}
+
+// a2 with the mean-key rows of the first chunk loaded into registers up front
+// (before the caller's a1 and q staging, so those latencies overlap): octet o of
+// the block holds rows o + NO*u, u < U (NO = octets in the block).  Row
+// `fresh_i` (recomputed by a1 after the prefetch) is taken from `fresh` (smem).
+template <int D, int G, int U>
+struct ScorePrefetch {
+  static constexpr int FPL = D / 8;                // floats per octet lane
+  static constexpr int NV = FPL >= 4 ? FPL / 4 : 1;
+  float4 kv[U][NV];
+  float2 kv2[U];
+  __device__ __forceinline__ void load(const float *__restrict__ mk, int nt, int base) {
+    const int lane = threadIdx.x & 31, oct = (threadIdx.x >> 3), l8 = lane & 7;
+    const int NO = blockDim.x >> 3;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + oct + NO * u;
+      const float *row = mk + (int64_t)(i < nt ? i : 0) * D;
+      if constexpr (FPL >= 4) {
+#pragma unroll
+        for (int m = 0; m < NV; ++m) kv[u][m] = __ldcg(reinterpret_cast<const float4 *>(row + m * 32 + l8 * 4));
+      } else {
+        kv2[u] = __ldcg(reinterpret_cast<const float2 *>(row + l8 * 2));
+      }
+    }
+  }
+  // alphas of the chunk into al[hh*ald + i] (and alpha_out)
+  __device__ __forceinline__ void compute(const float *qs, int nt, int base, int fresh_i, const float *fresh, float *al,
+                                          int ald, float *__restrict__ alpha_out, int64_t ald_out) {
+    const int lane = threadIdx.x & 31, oct = (threadIdx.x >> 3), l8 = lane & 7;
+    const int NO = blockDim.x >> 3;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + oct + NO * u;
+      if (i == fresh_i) {  // a1 just rewrote this row: use its value, not the prefetched one
+        if constexpr (FPL >= 4) {
+#pragma unroll
+          for (int m = 0; m < NV; ++m) kv[u][m] = *reinterpret_cast<const float4 *>(fresh + m * 32 + l8 * 4);
+        } else {
+          kv2[u] = *reinterpret_cast<const float2 *>(fresh + l8 * 2);
+        }
+      }
+      float acc[G];
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        float a = 0.f;
+        if constexpr (FPL >= 4) {
+#pragma unroll
+          for (int m = 0; m < NV; ++m) {
+            const float4 qv = *reinterpret_cast<const float4 *>(qs + hh * D + m * 32 + l8 * 4);
+            a = fmaf(kv[u][m].x, qv.x, a);
+            a = fmaf(kv[u][m].y, qv.y, a);
+            a = fmaf(kv[u][m].z, qv.z, a);
+            a = fmaf(kv[u][m].w, qv.w, a);
+          }
+        } else {
+          const float2 qv = *reinterpret_cast<const float2 *>(qs + hh * D + l8 * 2);
+          a = fmaf(kv2[u].x, qv.x, a);
+          a = fmaf(kv2[u].y, qv.y, a);
+        }
+        a += __shfl_xor_sync(0xffffffffu, a, 4);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        acc[hh] = a;
+      }
+      if (i < nt) {
+#pragma unroll
+        for (int hh = 0; hh < G; ++hh)
+          if (l8 == hh) {
+            al[hh * ald + i] = acc[hh];
+            if (alpha_out) alpha_out[hh * ald_out + i] = acc[hh];
+          }
+      }
+    }
+  }
+};
+
+// per-voter top-k over al (smem) for the G voters of the block: warp hh < G
+__device__ __forceinline__ void block_topk_voters(int G, float *al, int ald, int nt, int top_k, int *sel_i,
+                                                  float *sel_a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int kk = top_k < nt ? top_k : nt;
+  for (int hh = warp; hh < G; hh += nw) {
+    float *a = al + hh * ald;
+    for (int r = 0; r < kk; ++r) {
+      float ba = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int i = lane; i < nt; i += 32) {
+        const float x = a[i];
+        if (better_alpha(x, i, ba, bi)) { ba = x; bi = i; }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const float oa = __shfl_xor_sync(0xffffffffu, ba, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (better_alpha(oa, oi, ba, bi)) { ba = oa; bi = oi; }
+      }
+      if (lane == 0) {
+        sel_i[hh * top_k + r] = bi;
+        sel_a[hh * top_k + r] = ba;
+        a[bi] = -INFINITY;  // exclude from the next round
+      }
+      __syncwarp();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- a3 -----
@@ -347,11 +454,24 @@ static __device__ void block_topc(const int *v, const long long *A, int nt, int 
 // One pass reads the segment table (validation + clipped piece extents into
 // shared memory), a block scan turns lengths into offsets, and the fill reads
 // only shared memory: one warp per piece, coalesced stores.
+// With `phys` non-null, also writes the page-resolved row of every entry,
+// phys[j] = pt[t/P] * HkvP + t%P (HkvP = H_kv*P), so that a5 needs no page-table
+// lookup: row(l, g, t) = (l*num_pages*H_kv + g)*P + phys.  `pt` is the sequence's
+// page table (shared or global memory).
 static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][4] */, int nt, int T,
                                          const uint8_t *fl, int sink, int window, int32_t *__restrict__ out,
                                          int cap, int32_t *__restrict__ count_out,
                                          int *piece /* smem [2*nt]: start, then offset */,
-                                         int *scratch /* smem >= 33 ints */, int32_t *status) {
+                                         int *scratch /* smem >= 33 ints */, int32_t *status,
+                                         int32_t *__restrict__ phys = nullptr, const int32_t *pt = nullptr,
+                                         int P = 1, int HkvP = 1) {
+  auto emit = [&](int j, int t) {
+    out[j] = t;
+    if (phys) {
+      const int lp = t / P;
+      phys[j] = pt[lp] * HkvP + (t - lp * P);
+    }
+  };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int sp = sink < T ? sink : T;                  // s'
   const int w0 = (T - window > sp) ? T - window : sp;  // start of the window piece
@@ -387,10 +507,10 @@ static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][
     if (count > cap) set_status(status, ZOOMR_ERR_CAPACITY);
     *count_out = count < cap ? count : cap;
   }
-  for (int j = tid; j < sp && j < cap; j += blockDim.x) out[j] = j;  // sink
+  for (int j = tid; j < sp && j < cap; j += blockDim.x) emit(j, j);  // sink
   const int wbase = sp + total;
   for (int j = tid; j < T - w0; j += blockDim.x)                      // window
-    if (wbase + j < cap) out[wbase + j] = w0 + j;
+    if (wbase + j < cap) emit(wbase + j, w0 + j);
   // one warp per piece; a warp's pieces are fetched into registers up front
   // (lane u holds piece warp + u*nwarps) so the fill loop has no shared-memory
   // round trip per piece
@@ -409,7 +529,7 @@ static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][
       const int len = __shfl_sync(0xffffffffu, mlen, u);
       if (a < 0) continue;
       for (int j = lane; j < len; j += 32)
-        if (base + j < cap) out[base + j] = a + j;
+        if (base + j < cap) emit(base + j, a + j);
     }
   }
 }

@@ -80,6 +80,7 @@ struct AttnParams {
   const int32_t *page_table;
   int32_t max_pages;
   const int32_t *index;
+  const int32_t *index_phys;  // nullable: page-resolved rows written by the fused select
   const int32_t *count;
   int32_t cap;
   float *out;
@@ -261,12 +262,14 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       a.g = seg - a.l * p.Hkv;
       const int pos = tis * kTile + lane;
       a.ok = pos < cnt;
-      a.tok = a.ok ? p.index[(int64_t)a.b * p.cap + pos] : 0;
+      // with index_phys, `tok` carries the page-resolved row and stage B is a no-op
+      const int32_t *src = p.index_phys ? p.index_phys : p.index;
+      a.tok = a.ok ? src[(int64_t)a.b * p.cap + pos] : 0;
     };
     auto stage_b = [&](Addr &a) {
       a.page = 0;
       a.slot = 0;
-      if (a.ok) {
+      if (a.ok && !p.index_phys) {
         const int lp = p.Pshift >= 0 ? (a.tok >> p.Pshift) : a.tok / p.P;
         a.slot = a.tok - lp * p.P;
         if (a.tok >= 0 && lp < p.max_pages) a.page = p.page_table[(int64_t)a.b * p.max_pages + lp];
@@ -290,17 +293,28 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       Addr &ac = q0;
       // stage C: global row of every token of tile k
       const int cok = ac.ok;
+      int64_t grow = 0;
       int page = ac.page;
-      if (cok && (page < 0 || page >= p.num_pages)) {
-        set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
-        page = 0;
+      if (p.index_phys) {
+        // row(l, g, t) = (l*num_pages*H_kv + g)*P + phys(t); consecutive phys = contiguous rows
+        int phys = ac.tok;
+        if (cok && (phys < 0 || (int64_t)phys >= p.num_pages * p.Hkv * p.P)) {
+          set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+          phys = 0;
+        }
+        if (cok) grow = ((int64_t)ac.l * p.num_pages * p.Hkv + ac.g) * p.P + phys;
+      } else {
+        if (cok && (page < 0 || page >= p.num_pages)) {
+          set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
+          page = 0;
+        }
+        if (cok) grow = (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot;
       }
-      const int64_t grow = cok ? (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot : 0;
       // runs of consecutive tokens in one page -> boxes of 16 / 8 rows; the rest by cp.async
       const int ptok = __shfl_up_sync(0xffffffffu, ac.tok, 1);
       const int ppage = __shfl_up_sync(0xffffffffu, page, 1);
       const int pok = __shfl_up_sync(0xffffffffu, cok, 1);
-      const bool cont = cok && lane > 0 && pok && ptok + 1 == ac.tok && ppage == page;
+      const bool cont = cok && lane > 0 && pok && ptok + 1 == ac.tok && (p.index_phys || ppage == page);
       const unsigned validm = __ballot_sync(0xffffffffu, cok);
       const unsigned startm = __ballot_sync(0xffffffffu, cok && !cont);
       const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
@@ -372,7 +386,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   constexpr bool kTwoN = (G == 8);          // hi and lo in separate n-tiles
   // column -> (head, part) for G <= 4: head = n % G, part = n / G (0 hi, 1 lo, >=2 none)
   const int part0 = kTwoN ? 0 : n0 / G, part1 = kTwoN ? 0 : (n0 + 1) / G;
-  constexpr int SLOT = G * (D + 2);  // partial result: m[G], l[G], O[G][D]
+  constexpr int HDR = (2 * G + 3) / 4 * 4;  // m[G], l[G] padded to a 16-byte boundary
+  constexpr int SLOT = HDR + G * D;         // partial result: header, then O[G][D]
 
   int first_b = -1, first_seg = -1;  // the first segment of this warp's range (slot rule)
   int cur_b = -1, cur_seg = -1;
@@ -444,11 +459,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
 #pragma unroll
       for (int me = 0; me < NKS; ++me) {
         const int e = me * 16 + gq;
-        ps[2 * G + n0 * D + e] = ov[me][0];
-        ps[2 * G + n0 * D + e + 8] = ov[me][2];
+        ps[HDR + n0 * D + e] = ov[me][0];
+        ps[HDR + n0 * D + e + 8] = ov[me][2];
         if (nh == 2) {
-          ps[2 * G + (n0 + 1) * D + e] = ov[me][1];
-          ps[2 * G + (n0 + 1) * D + e + 8] = ov[me][3];
+          ps[HDR + (n0 + 1) * D + e] = ov[me][1];
+          ps[HDR + (n0 + 1) * D + e + 8] = ov[me][3];
         }
       }
     }
@@ -460,57 +475,80 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != (int)(wl - wf)) return;  // not the last arriving warp
     __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
-    // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic)
+    // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic).
+    // Lane j fetches part j's header (slot pointer, m[G], l[G]) so that all the
+    // round trips of a chunk of 32 parts are in flight together.
     const int nparts = (int)(wl - wf + 1);
+    constexpr int NV4 = G * D / 4;
+    constexpr int PER = (NV4 + 31) / 32;
     float Mh[G], Lh[G];
+    float4 acc[PER];
 #pragma unroll
-    for (int h = 0; h < G; ++h) Mh[h] = -INFINITY;
-    // pass 1 (lane-parallel over parts): per-head max
-    for (int j0 = 0; j0 < nparts; j0 += 32) {
-      const int j = j0 + lane;
-      if (j < nparts) {
-        int fb, fs, ft, fn;
-        sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
-        const float *q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
+    for (int h = 0; h < G; ++h) {
+      Mh[h] = -INFINITY;
+      Lh[h] = 0.f;
+    }
 #pragma unroll
-        for (int h = 0; h < G; ++h) Mh[h] = fmaxf(Mh[h], __ldcg(q2 + h));
+    for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j0 = 0; j0 < nparts; j0 += 32) {
+        const int j = j0 + lane;
+        const float *q2 = nullptr;
+        float mj[G], lj[G];
+        if (j < nparts) {
+          int fb, fs, ft, fn;
+          sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
+          q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            mj[h] = __ldcg(q2 + h);
+            lj[h] = __ldcg(q2 + G + h);
+          }
+        }
+        if (pass == 0) {  // per-head max over all parts
+          if (j < nparts)
+#pragma unroll
+            for (int h = 0; h < G; ++h) Mh[h] = fmaxf(Mh[h], mj[h]);
+          continue;
+        }
+        float wj[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          wj[h] = j < nparts ? ex2(mj[h] - Mh[h]) : 0.f;
+          Lh[h] += j < nparts ? lj[h] * wj[h] : 0.f;
+        }
+        const int nj = min(32, nparts - j0);
+        for (int u0 = 0; u0 < nj; ++u0) {
+          const float *qq = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)q2, u0);
+          float w[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) w[h] = __shfl_sync(0xffffffffu, wj[h], u0);
+          const float4 *O4 = reinterpret_cast<const float4 *>(qq + HDR);
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int f = lane + 32 * u;
+            if (f < NV4) {
+              const float4 v = __ldcg(O4 + f);
+              const float ww = w[(4 * f) / D];
+              acc[u].x += v.x * ww;
+              acc[u].y += v.y * ww;
+              acc[u].z += v.z * ww;
+              acc[u].w += v.w * ww;
+            }
+          }
+        }
+      }
+      if (pass == 0) {
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int off = 16; off; off >>= 1) Mh[h] = fmaxf(Mh[h], __shfl_xor_sync(0xffffffffu, Mh[h], off));
       }
     }
 #pragma unroll
     for (int h = 0; h < G; ++h)
 #pragma unroll
-      for (int off = 16; off; off >>= 1) Mh[h] = fmaxf(Mh[h], __shfl_xor_sync(0xffffffffu, Mh[h], off));
-    // pass 2: rescaled sums; lane-parallel over float4 of O[G][D]
-    constexpr int NV4 = G * D / 4;
-    constexpr int PER = (NV4 + 31) / 32;
-    float4 acc[PER];
-#pragma unroll
-    for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int h = 0; h < G; ++h) Lh[h] = 0.f;
-    for (int j = 0; j < nparts; ++j) {
-      int fb, fs, ft, fn;
-      sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
-      const float *q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
-      float w[G];
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        w[h] = ex2(__ldcg(q2 + h) - Mh[h]);
-        Lh[h] += __ldcg(q2 + G + h) * w[h];
-      }
-      const float *O = q2 + 2 * G;
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int f = lane + 32 * u;
-        if (f < NV4) {
-          const float ww = w[(4 * f) / D];
-          acc[u].x += __ldcg(O + 4 * f + 0) * ww;
-          acc[u].y += __ldcg(O + 4 * f + 1) * ww;
-          acc[u].z += __ldcg(O + 4 * f + 2) * ww;
-          acc[u].w += __ldcg(O + 4 * f + 3) * ww;
-        }
-      }
-    }
+      for (int off = 16; off; off >>= 1) Lh[h] += __shfl_xor_sync(0xffffffffu, Lh[h], off);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int f = lane + 32 * u;
@@ -686,7 +724,7 @@ inline int encode_pool_map(CUtensorMap *m, const void *base, int d, uint64_t row
 
 inline size_t attn_ws_part_floats(const zoomr_geom *g) {
   const int G = g->num_q_heads / g->num_kv_heads;
-  return (size_t)attn_grid() * kPairs * 2 * G * (g->head_dim + 2);
+  return (size_t)attn_grid() * kPairs * 2 * ((2 * G + 3) / 4 * 4 + G * g->head_dim);
 }
 
 }  // namespace zoomr
@@ -701,7 +739,7 @@ extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t bat
 }
 
 extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
-                                        const zoomr_kv *kv, const int32_t *index,
+                                        const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                         const int32_t *index_count, int32_t index_capacity,
                                         float softmax_scale, float *out, void *workspace,
                                         size_t workspace_bytes, int32_t *dev_status, void *stream) {
@@ -721,6 +759,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   prm.page_table = kv->page_table;
   prm.max_pages = kv->max_pages;
   prm.index = index;
+  prm.index_phys = index_phys;
   prm.count = index_count;
   prm.cap = index_capacity;
   prm.out = out;

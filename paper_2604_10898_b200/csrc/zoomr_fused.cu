@@ -47,6 +47,7 @@ struct FusedParams {
   uint8_t *flags;
   float *agreeability;    // nullable
   int32_t *index;
+  int32_t *index_phys;    // nullable: page-resolved rows for a5
   int32_t cap;
   int32_t *count;
   float *alpha_out;       // nullable
@@ -56,6 +57,8 @@ struct FusedParams {
   int32_t *ws_ticket;     // [B]
   int32_t L, Hkv, P;
   int32_t *status;
+  int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
+  int32_t variant;     // debug A/B only: a2 implementation
 };
 
 template <int D, int G>
@@ -104,7 +107,25 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     float *sel_a = reinterpret_cast<float *>(sel_i + G * p.top_k);   // [G][k]
     const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
     float *ao = p.alpha_out ? p.alpha_out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * MS : nullptr;
-    block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
+    if (p.variant == 0) {
+      block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
+    } else {
+      // variant 1: all rows of the first chunk loaded up front (U per octet), q staged meanwhile
+      constexpr int U = 4;
+      ScorePrefetch<D, G, U> pf;
+      const int chunk = (blockDim.x >> 3) * U;
+      pf.load(mk, nt, 0);
+      for (int x = threadIdx.x; x < G * D; x += blockDim.x) qs[x] = __bfloat162float(qb[x]);
+      __syncthreads();
+      pf.compute(qs, nt, 0, -1, nullptr, al, MS, ao, MS);
+      for (int base = chunk; base < nt; base += chunk) {
+        pf.load(mk, nt, base);
+        pf.compute(qs, nt, base, -1, nullptr, al, MS, ao, MS);
+      }
+      __syncthreads();
+      block_topk_voters(G, al, MS, nt, p.top_k, sel_i, sel_a);
+      __syncthreads();
+    }
     const int kk = p.top_k < nt ? p.top_k : nt;
     for (int x = threadIdx.x; x < G * p.top_k; x += blockDim.x) {
       const int hh = x / p.top_k, r = x - hh * p.top_k;
@@ -128,6 +149,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   }
   __syncthreads();
   if (!ticket_last) return;
+  if (p.stop_after == 1) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
 
   // ---- aggregation (a2, cross-head / cross-layer), exact integer atomics --------
   SmemCarve sm{smem_raw};
@@ -137,7 +159,10 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   int *hist = sm.take<int>(kHistBins);
   int *scratch = sm.take<int>(40);
   int4 *bds = sm.take<int4>(MS);        // segment table of b
+  int *pts = sm.take<int>(p.max_pages); // page table of b (for index_phys)
   uint8_t *fl = sm.take<uint8_t>(MS);
+  if (p.index_phys)
+    for (int x = threadIdx.x; x < p.max_pages; x += blockDim.x) pts[x] = p.page_table[(int64_t)b * p.max_pages + x];
   // collect the aggregate (leaving the accumulators zeroed for the next call)
   // and stage the segment table for a4
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
@@ -155,12 +180,14 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
       pv[MS + i] = i < nt ? A[i] : 0;
     }
   }
+  if (p.stop_after == 2) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
   // ---- a3: consensus top-c ----------------------------------------------------------
   block_topc(v, A, nt, p.c, fl, hist, grp, scratch, p.agreeability ? p.agreeability + b : nullptr);
 
   uint8_t *fo = p.flags + (int64_t)b * MS;
   for (int i = threadIdx.x; i < MS; i += blockDim.x) fo[i] = i < nt ? fl[i] : 0;
   __syncthreads();
+  if (p.stop_after == 3) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
   // ---- a4: the index set --------------------------------------------------------------
   if (T < 1) {
     if (threadIdx.x == 0) {
@@ -168,18 +195,19 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
       p.count[b] = 0;
     }
   } else {
-    block_build_index(reinterpret_cast<const int32_t *>(bds), nt, T, fl, p.sink, p.window, p.index + (int64_t)b * p.cap, p.cap, p.count + b, grp,
-                      scratch, p.status);
+    block_build_index(reinterpret_cast<const int32_t *>(bds), nt, T, fl, p.sink, p.window, p.index + (int64_t)b * p.cap,
+                      p.cap, p.count + b, grp, scratch, p.status,
+                      p.index_phys ? p.index_phys + (int64_t)b * p.cap : nullptr, pts, p.P, p.Hkv * p.P);
   }
   if (threadIdx.x == 0) p.ws_ticket[b] = 0;  // ready for the next step
   __syncthreads();
 }
 
 template <int D, int G>
-size_t fused_smem_bytes(int MS, int top_k) {
+size_t fused_smem_bytes(int MS, int top_k, int max_pages) {
   const size_t a1 = 8 * (256 / 32) * D;
   const size_t a2 = (size_t)G * D * 4 + (size_t)G * MS * 4 + (size_t)G * top_k * 8;
-  const size_t a3 = (size_t)MS * (8 + 4 + 8 + 16 + 1) + (kHistBins + 40) * 4 + 8 * 16;
+  const size_t a3 = (size_t)MS * (8 + 4 + 8 + 16 + 1) + (kHistBins + 40) * 4 + (size_t)max_pages * 4 + 9 * 16;
   return a1 > a2 ? (a1 > a3 ? a1 : a3) : (a2 > a3 ? a2 : a3);
 }
 
@@ -196,7 +224,7 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
                                   const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
                                   float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
                                   int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
-                                  int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                                  int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
                                   int32_t *topk_out, void *workspace, size_t workspace_bytes,
                                   int32_t *dev_status, void *stream) {
   int rc = check_geom(geom);
@@ -229,6 +257,7 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   p.flags = flags;
   p.agreeability = agreeability;
   p.index = index;
+  p.index_phys = index_phys;
   p.cap = index_capacity;
   p.count = index_count;
   p.alpha_out = alpha_out;
@@ -241,13 +270,19 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   p.Hkv = geom->num_kv_heads;
   p.P = geom->page_size;
   p.status = dev_status;
+  {
+    const char *e = getenv("ZOOMR_FUSED_STOP");
+    p.stop_after = e ? atoi(e) : 0;
+    const char *v = getenv("ZOOMR_FUSED_VARIANT");
+    p.variant = v ? atoi(v) : 0;
+  }
   const int G = geom->num_q_heads / geom->num_kv_heads;
   dim3 grid(geom->num_layers * geom->num_kv_heads, batch);
   cudaStream_t s = (cudaStream_t)stream;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
     auto kfn = fused_select_kernel<DD, GG>;                                                      \
-    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k);                     \
+    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, kv->max_pages);                     \
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     prefer_max_smem(kfn);                                                                        \

@@ -28,7 +28,7 @@ class ZoomrStep:
     """Device state + launch sequence of one (rank-local) decode step."""
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
-                 params: StepParams, device="cuda", debug_outputs: bool = False):
+                 params: StepParams, device="cuda", debug_outputs: bool = False, use_phys: bool = False):
         self.shape, self.batch, self.params = shape, batch, params
         self.max_summaries, self.cap = max_summaries, index_capacity
         dev = torch.device(device)
@@ -37,6 +37,7 @@ class ZoomrStep:
         self.partial = torch.zeros(batch, 2, max_summaries, dtype=torch.int64, device=dev)
         self.flags = torch.zeros(batch, max_summaries, dtype=torch.uint8, device=dev)
         self.index = torch.zeros(batch, index_capacity, dtype=torch.int32, device=dev)
+        self.index_phys = torch.zeros(batch, index_capacity, dtype=torch.int32, device=dev)
         self.count = torch.zeros(batch, dtype=torch.int32, device=dev)
         self.out = torch.zeros(batch, L, Hq, d, dtype=torch.float32, device=dev)
         self.agreeability = torch.zeros(batch, dtype=torch.float32, device=dev)
@@ -50,6 +51,7 @@ class ZoomrStep:
             self.alpha = torch.zeros(batch, L, Hq, max_summaries, dtype=torch.float32, device=dev)
             self.topk = torch.zeros(batch, L * Hq, params.top_k, dtype=torch.int32, device=dev)
         self.graph = None
+        self.use_phys = use_phys  # fused select writes page-resolved rows for a5
 
     # -- a1: mean keys for a list of closed summaries (b, i) --------------------
     def update_mean_keys(self, kv, seg, items: torch.Tensor):
@@ -86,9 +88,10 @@ class ZoomrStep:
                            self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags, self.index,
                            self.count, self.sel_workspace, partial=self.partial,
                            agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
-                           dev_status=self.status)
+                           dev_status=self.status, index_phys=self.index_phys if self.use_phys else None)
             Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
-                                 self.out, self.workspace, dev_status=self.status)
+                                 self.out, self.workspace, dev_status=self.status,
+                                 index_phys=self.index_phys if self.use_phys else None)
             return self.out
         if close_items is not None and close_items.numel():
             self.update_mean_keys(kv, seg, close_items)

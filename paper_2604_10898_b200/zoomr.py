@@ -65,12 +65,12 @@ def lib():
         L.zoomr_build_index.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]
         L.zoomr_attn_workspace_bytes.argtypes = [vp, i32]
         L.zoomr_attn_workspace_bytes.restype = sz
-        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, i32, C.c_float, vp, vp, sz,
+        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, vp, vp, sz,
                                                vp, vp]
         L.zoomr_select_workspace_bytes.argtypes = [vp, i32, i32]
         L.zoomr_select_workspace_bytes.restype = sz
         L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp,
-                                         vp, i32, vp, vp, vp, vp, sz, vp, vp]
+                                         vp, vp, i32, vp, vp, vp, vp, sz, vp, vp]
         L.zoomr_select_fused.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
@@ -190,12 +190,13 @@ def attn_workspace_bytes(shape: Shape, batch: int) -> int:
 
 
 def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out,
-                       workspace, softmax_scale=None, dev_status=None, stream=None):
+                       workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None):
     """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
     rc = lib().zoomr_sparse_decode_attn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
                                         C.byref(kv), _ptr(index, torch.int32, "index"),
+                                        _ptr(index_phys, torch.int32, "index_phys"),
                                         _ptr(index_count, torch.int32, "index_count"), index.shape[1],
                                         C.c_float(sc), _ptr(out, torch.float32, "out"),
                                         _ptr(workspace, None, "workspace"), workspace.numel() *
@@ -211,7 +212,8 @@ def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:
 
 def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summaries, seq_len, close_items,
                  mean_keys, top_k, c, sink, window, flags, index, index_count, workspace, partial=None,
-                 agreeability=None, alpha_out=None, topk_out=None, dev_status=None, stream=None):
+                 agreeability=None, alpha_out=None, topk_out=None, dev_status=None, stream=None,
+                 index_phys=None):
     """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None."""
     g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
     n_close = 0 if close_items is None else close_items.shape[0]
@@ -220,7 +222,8 @@ def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summar
         _ptr(close_items, torch.int32, "close_items") if n_close else None, n_close,
         _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k), int(c), int(sink), int(window),
         _ptr(partial, torch.int64, "partial"), _ptr(flags, torch.uint8, "flags"),
-        _ptr(agreeability, torch.float32, "agreeability"), _ptr(index, torch.int32, "index"), index.shape[1],
+        _ptr(agreeability, torch.float32, "agreeability"), _ptr(index, torch.int32, "index"),
+        _ptr(index_phys, torch.int32, "index_phys"), index.shape[1],
         _ptr(index_count, torch.int32, "index_count"), _ptr(alpha_out, torch.float32, "alpha_out"),
         _ptr(topk_out, torch.int32, "topk_out"), _ptr(workspace, None, "workspace"),
         workspace.numel() * workspace.element_size(), _ptr(dev_status, torch.int32, "dev_status"),

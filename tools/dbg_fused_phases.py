@@ -1,5 +1,5 @@
 import ctypes as C, torch, sys
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import zoomr_synth as S
 from tests import parity as PY
 from paper_2604_10898_b200 import zoomr as Z
@@ -12,10 +12,11 @@ lib = Z.lib()
 for rep in range(5):
     torch.cuda.synchronize()
     Z.select_fused(st.shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, inp.bounds, inp.num_summaries, inp.seq_len,
-                   newest, st.mean_keys, 2, 4, 4, 512, st.flags, st.index, st.count, st.sel_workspace, partial=st.partial)
+                   newest, st.mean_keys, 2, 4, 4, 512, st.flags, st.index, st.count, st.sel_workspace, partial=st.partial,
+                   index_phys=None)
     torch.cuda.synchronize()
-    buf = (C.c_ulonglong * 16)()
+    buf = (C.c_ulonglong * 32)()
     lib.zoomr_debug_timestamps(buf)
     t = list(buf)
-    b0 = t[0]
-    print("cta0:", [ (x - b0) for x in t[0:3]], " last:", [(x - b0) if x else None for x in t[8:15]])
+    base = min(x for x in t if x)
+    print("last:", [round((x - base)/1000, 2) if x else None for x in t[16:32]])

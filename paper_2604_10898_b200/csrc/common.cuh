@@ -69,8 +69,13 @@ inline void launch_pdl(Kern kfn, int grid, int block, size_t smem, cudaStream_t 
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static int no_pdl = -1;
+  if (no_pdl < 0) {
+    const char *e = getenv("ZOOMR_NO_PDL");  // A/B experiments only
+    no_pdl = e ? atoi(e) : 0;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   cudaLaunchKernelEx(&cfg, kfn, args...);
 }
 

@@ -220,82 +220,6 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
   __syncthreads();
 }
 
-// a2 with the mean-key rows of the first chunk loaded into registers up front
-// (before the caller's a1 and q staging, so those latencies overlap): octet o of
-// the block holds rows o + NO*u, u < U (NO = octets in the block).  Row
-// `fresh_i` (recomputed by a1 after the prefetch) is taken from `fresh` (smem).
-template <int D, int G, int U>
-struct ScorePrefetch {
-  static constexpr int FPL = D / 8;                // floats per octet lane
-  static constexpr int NV = FPL >= 4 ? FPL / 4 : 1;
-  float4 kv[U][NV];
-  float2 kv2[U];
-  __device__ __forceinline__ void load(const float *__restrict__ mk, int nt, int base) {
-    const int lane = threadIdx.x & 31, oct = (threadIdx.x >> 3), l8 = lane & 7;
-    const int NO = blockDim.x >> 3;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + oct + NO * u;
-      const float *row = mk + (int64_t)(i < nt ? i : 0) * D;
-      if constexpr (FPL >= 4) {
-#pragma unroll
-        for (int m = 0; m < NV; ++m) kv[u][m] = __ldcg(reinterpret_cast<const float4 *>(row + m * 32 + l8 * 4));
-      } else {
-        kv2[u] = __ldcg(reinterpret_cast<const float2 *>(row + l8 * 2));
-      }
-    }
-  }
-  // alphas of the chunk into al[hh*ald + i] (and alpha_out)
-  __device__ __forceinline__ void compute(const float *qs, int nt, int base, int fresh_i, const float *fresh, float *al,
-                                          int ald, float *__restrict__ alpha_out, int64_t ald_out) {
-    const int lane = threadIdx.x & 31, oct = (threadIdx.x >> 3), l8 = lane & 7;
-    const int NO = blockDim.x >> 3;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + oct + NO * u;
-      if (i == fresh_i) {  // a1 just rewrote this row: use its value, not the prefetched one
-        if constexpr (FPL >= 4) {
-#pragma unroll
-          for (int m = 0; m < NV; ++m) kv[u][m] = *reinterpret_cast<const float4 *>(fresh + m * 32 + l8 * 4);
-        } else {
-          kv2[u] = *reinterpret_cast<const float2 *>(fresh + l8 * 2);
-        }
-      }
-      float acc[G];
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        float a = 0.f;
-        if constexpr (FPL >= 4) {
-#pragma unroll
-          for (int m = 0; m < NV; ++m) {
-            const float4 qv = *reinterpret_cast<const float4 *>(qs + hh * D + m * 32 + l8 * 4);
-            a = fmaf(kv[u][m].x, qv.x, a);
-            a = fmaf(kv[u][m].y, qv.y, a);
-            a = fmaf(kv[u][m].z, qv.z, a);
-            a = fmaf(kv[u][m].w, qv.w, a);
-          }
-        } else {
-          const float2 qv = *reinterpret_cast<const float2 *>(qs + hh * D + l8 * 2);
-          a = fmaf(kv2[u].x, qv.x, a);
-          a = fmaf(kv2[u].y, qv.y, a);
-        }
-        a += __shfl_xor_sync(0xffffffffu, a, 4);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        acc[hh] = a;
-      }
-      if (i < nt) {
-#pragma unroll
-        for (int hh = 0; hh < G; ++hh)
-          if (l8 == hh) {
-            al[hh * ald + i] = acc[hh];
-            if (alpha_out) alpha_out[hh * ald_out + i] = acc[hh];
-          }
-      }
-    }
-  }
-};
-
 // per-voter top-k over al (smem) for the G voters of the block: warp hh < G
 __device__ __forceinline__ void block_topk_voters(int G, float *al, int ald, int nt, int top_k, int *sel_i,
                                                   float *sel_a) {

@@ -44,6 +44,7 @@ namespace zoomr {
 constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addresses)
 constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
 constexpr int kStages = 3;  // ring depth per pair
+constexpr int kPtSmem = 4096; // page-table entries staged in shared memory when they fit
 
 template <int D>
 struct AttnShape {
@@ -87,6 +88,7 @@ struct AttnParams {
   float *ws_part;  // [NW][2][G*(D+2)]
   int32_t *ws_cnt; // [B*L*Hkv]
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
+  int32_t pt_smem;               // page table staged in shared memory (B*max_pages <= kPtSmem)
   float scale_log2;
   int32_t *status;
 };
@@ -188,7 +190,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   unsigned char *smem = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kPairs][kStages]
   uint64_t *empty = full + kPairs * kStages;                             // [kPairs][kStages]
-  int32_t *prefix = reinterpret_cast<int32_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // [B+1]
+  int32_t *pts = reinterpret_cast<int32_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // [kPtSmem] page tables
+  int32_t *prefix = pts + (p.pt_smem ? kPtSmem : 0);                                  // [B+1]
+  int32_t *cnts = prefix + p.B + 1;                                                   // [B] clamped |I_f|
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
 
@@ -199,6 +203,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // The page tables are inputs, not outputs of the preceding kernel (a4 / the
+  // fused select): stage them while that kernel is still finishing.
+  if (p.pt_smem)
+    for (int x = threadIdx.x; x < p.B * p.max_pages; x += blockDim.x) pts[x] = p.page_table[x];
   // Programmatic dependent launch: everything above overlaps the producer of
   // I_f (a4 / the fused select); from here on its results are visible.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -211,6 +219,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       if (b < p.B) {
         int c = p.count[b];
         c = c < p.cap ? c : p.cap;
+        cnts[b] = c;
         n = c > 0 ? (c + kTile - 1) / kTile * p.L * p.Hkv : 0;
       }
       int incl = n;
@@ -256,15 +265,15 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     auto stage_a = [&](int64_t k, Addr &a) {
       int seg, tis, nts;
       sc.locate(r0 + k, a.b, seg, tis, nts);
-      int cnt = p.count[a.b];
-      cnt = cnt < p.cap ? cnt : p.cap;
+      const int cnt = cnts[a.b];
       a.l = seg / p.Hkv;
       a.g = seg - a.l * p.Hkv;
       const int pos = tis * kTile + lane;
       a.ok = pos < cnt;
-      // with index_phys, `tok` carries the page-resolved row and stage B is a no-op
+      // with index_phys, `tok` carries the page-resolved row and stage B is a no-op;
+      // the load is guarded by the capacity, not the count, so it does not wait for it
       const int32_t *src = p.index_phys ? p.index_phys : p.index;
-      a.tok = a.ok ? src[(int64_t)a.b * p.cap + pos] : 0;
+      a.tok = pos < p.cap ? src[(int64_t)a.b * p.cap + pos] : 0;
     };
     auto stage_b = [&](Addr &a) {
       a.page = 0;
@@ -272,7 +281,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       if (a.ok && !p.index_phys) {
         const int lp = p.Pshift >= 0 ? (a.tok >> p.Pshift) : a.tok / p.P;
         a.slot = a.tok - lp * p.P;
-        if (a.tok >= 0 && lp < p.max_pages) a.page = p.page_table[(int64_t)a.b * p.max_pages + lp];
+        if (a.tok >= 0 && lp < p.max_pages)
+          a.page = p.pt_smem ? pts[a.b * p.max_pages + lp] : p.page_table[(int64_t)a.b * p.max_pages + lp];
         else a.page = -1;
       }
     };
@@ -280,16 +290,19 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     // kAheadB tiles ahead of the copies
     constexpr int kAheadA = 4, kAheadB = 2;
     Addr q0{}, q1{}, q2{}, q3{}, q4{};  // tiles k .. k+4
-    if (ntiles > 0) stage_a(0, q0);
-    if (ntiles > 1) stage_a(1, q1);
-    if (ntiles > 2) stage_a(2, q2);
-    if (ntiles > 3) stage_a(3, q3);
-    if (ntiles > 0) stage_b(q0);
-    if (ntiles > 1) stage_b(q1);
     const int rsub = lane / S::CPR, ch = lane % S::CPR;
-    for (int64_t k = 0; k < ntiles; ++k) {
+    // one loop, one call site per stage (the pipeline fill is its first kAheadA
+    // iterations): the kernel's code stays small enough for the instruction cache
+    for (int64_t k = -kAheadA; k < ntiles; ++k) {
       if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
-      if (k + kAheadB < ntiles) stage_b(q2);
+      if (k + kAheadB >= 0 && k + kAheadB < ntiles) stage_b(q2);
+      if (k < 0) {
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = q4;
+        continue;
+      }
       Addr &ac = q0;
       // stage C: global row of every token of tile k
       const int cok = ac.ok;
@@ -476,11 +489,72 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     if (old != (int)(wl - wf)) return;  // not the last arriving warp
     __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
     // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic).
-    // Lane j fetches part j's header (slot pointer, m[G], l[G]) so that all the
-    // round trips of a chunk of 32 parts are in flight together.
     const int nparts = (int)(wl - wf + 1);
     constexpr int NV4 = G * D / 4;
     constexpr int PER = (NV4 + 31) / 32;
+    constexpr int NPF = G >= 8 ? 2 : 4;  // fast path: every load of up to NPF parts in flight at once
+    if (nparts <= NPF) {
+      const float *qp[NPF];
+      float mh[NPF][G], lh[NPF][G];
+      float4 ov4[NPF][PER];
+#pragma unroll
+      for (int j = 0; j < NPF; ++j) {
+        if (j < nparts) {
+          int fb, fs, ft, fn;
+          sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
+          qp[j] = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            mh[j][h] = __ldcg(qp[j] + h);
+            lh[j][h] = __ldcg(qp[j] + G + h);
+          }
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int f = lane + 32 * u;
+            ov4[j][u] = f < NV4 ? __ldcg(reinterpret_cast<const float4 *>(qp[j] + HDR) + f) : make_float4(0, 0, 0, 0);
+          }
+        }
+      }
+      float Mh[G], Lh[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        Mh[h] = -INFINITY;
+        Lh[h] = 0.f;
+#pragma unroll
+        for (int j = 0; j < NPF; ++j)
+          if (j < nparts) Mh[h] = fmaxf(Mh[h], mh[j][h]);
+      }
+      float w[NPF][G];
+#pragma unroll
+      for (int j = 0; j < NPF; ++j)
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          w[j][h] = j < nparts ? ex2(mh[j][h] - Mh[h]) : 0.f;
+          Lh[h] += j < nparts ? lh[j][h] * w[j][h] : 0.f;
+        }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int f = lane + 32 * u;
+        if (f < NV4) {
+          const int h = (4 * f) / D;
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < NPF; ++j)
+            if (j < nparts) {
+              a.x += ov4[j][u].x * w[j][h];
+              a.y += ov4[j][u].y * w[j][h];
+              a.z += ov4[j][u].z * w[j][h];
+              a.w += ov4[j][u].w * w[j][h];
+            }
+          const float inv = 1.f / Lh[h];
+          reinterpret_cast<float4 *>(ob)[f] = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+        }
+      }
+      if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
+      return;
+    }
+    // (general path) lane j fetches part j's header (slot pointer, m[G], l[G])
+    // so that all the round trips of a chunk of 32 parts are in flight together.
     float Mh[G], Lh[G];
     float4 acc[PER];
 #pragma unroll
@@ -561,15 +635,16 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
   };
 
-  for (int64_t k = 0; k < ntiles; ++k) {
-    int b, seg, tis, nts;
-    sc.locate(r0 + k, b, seg, tis, nts);
+  for (int64_t k = 0; k <= ntiles; ++k) {  // k == ntiles: only the final flush
+    int b = -1, seg = -1, tis = 0, nts = 0;
+    if (k < ntiles) sc.locate(r0 + k, b, seg, tis, nts);
     if (k == 0) {
       first_b = b;
       first_seg = seg;
     }
     if (b != cur_b || seg != cur_seg) {
       if (cur_b >= 0) flush(cur_b, cur_seg);
+      if (k == ntiles) break;
       cur_b = b;
       cur_seg = seg;
       // Q fragments (B operand of QK^T): Q[head n % G][k-chunk], this thread's column n = gq
@@ -590,8 +665,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
     }
-    int cnt = p.count[b];
-    cnt = cnt < p.cap ? cnt : p.cap;
+    const int cnt = cnts[b];
     const int nvalid = min(kTile, cnt - tis * kTile);
     const int s = (int)(k % kStages);
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
@@ -687,15 +761,22 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     __syncwarp();  // every lane is done reading the stage
     if (lane == 0) mbar_arrive(&emptyp[s]);
   }
-  if (cur_b >= 0) flush(cur_b, cur_seg);
 }
 
 template <int D, int G>
 size_t attn_smem_bytes(int B) {
-  return 1024 + (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)(B + 1) * sizeof(int32_t);
+  return 1024 + (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)kPtSmem * sizeof(int32_t) +
+         (size_t)(2 * B + 1) * sizeof(int32_t);
 }
 
-inline int attn_grid() { return num_sms(); }
+inline int attn_grid() {
+  static int spare = -1;
+  if (spare < 0) {
+    const char *e = getenv("ZOOMR_ATTN_SPARE_SMS");  // A/B experiments only
+    spare = e ? atoi(e) : 0;
+  }
+  return num_sms() - spare;
+}
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -770,6 +851,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   prm.L = geom->num_layers;
   prm.Hkv = geom->num_kv_heads;
   prm.P = geom->page_size;
+  prm.pt_smem = (int64_t)batch * kv->max_pages <= kPtSmem;
   prm.Pshift = -1;
   for (int sft = 0; sft < 31; ++sft)
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;

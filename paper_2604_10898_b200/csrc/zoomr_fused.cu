@@ -58,7 +58,6 @@ struct FusedParams {
   int32_t L, Hkv, P;
   int32_t *status;
   int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
-  int32_t variant;     // debug A/B only: a2 implementation
 };
 
 template <int D, int G>
@@ -107,25 +106,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     float *sel_a = reinterpret_cast<float *>(sel_i + G * p.top_k);   // [G][k]
     const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
     float *ao = p.alpha_out ? p.alpha_out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * MS : nullptr;
-    if (p.variant == 0) {
-      block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
-    } else {
-      // variant 1: all rows of the first chunk loaded up front (U per octet), q staged meanwhile
-      constexpr int U = 4;
-      ScorePrefetch<D, G, U> pf;
-      const int chunk = (blockDim.x >> 3) * U;
-      pf.load(mk, nt, 0);
-      for (int x = threadIdx.x; x < G * D; x += blockDim.x) qs[x] = __bfloat162float(qb[x]);
-      __syncthreads();
-      pf.compute(qs, nt, 0, -1, nullptr, al, MS, ao, MS);
-      for (int base = chunk; base < nt; base += chunk) {
-        pf.load(mk, nt, base);
-        pf.compute(qs, nt, base, -1, nullptr, al, MS, ao, MS);
-      }
-      __syncthreads();
-      block_topk_voters(G, al, MS, nt, p.top_k, sel_i, sel_a);
-      __syncthreads();
-    }
+    block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
     const int kk = p.top_k < nt ? p.top_k : nt;
     for (int x = threadIdx.x; x < G * p.top_k; x += blockDim.x) {
       const int hh = x / p.top_k, r = x - hh * p.top_k;
@@ -273,8 +254,6 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   {
     const char *e = getenv("ZOOMR_FUSED_STOP");
     p.stop_after = e ? atoi(e) : 0;
-    const char *v = getenv("ZOOMR_FUSED_VARIANT");
-    p.variant = v ? atoi(v) : 0;
   }
   const int G = geom->num_q_heads / geom->num_kv_heads;
   dim3 grid(geom->num_layers * geom->num_kv_heads, batch);

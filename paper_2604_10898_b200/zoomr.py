@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzoomr.so")
+LIB_PATH = os.environ.get("ZOOMR_LIB_OVERRIDE") or os.path.join(_HERE, "libzoomr.so")  # override: A/B builds only
 
 OK, ERR_INVALID_ARG, ERR_DIM_MISMATCH, ERR_EMPTY_SEGMENT, ERR_SEGMENT_ORDER, ERR_INDEX_RANGE, \
     ERR_CAPACITY, ERR_UNSUPPORTED, ERR_CUDA, ERR_WORKSPACE = range(10)

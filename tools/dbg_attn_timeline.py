@@ -18,5 +18,5 @@ for rep in range(4):
     base = min(x for x in t if x)
     names = ["start", "after_wait", "roles", "first_issue/first_wait", "first_done/first_data", "last_issue/loop_end", "flush_end"]
     for who, lab in [(0, "cta0 math"), (1, "cta0 prod"), (2, "cta77 math"), (3, "cta77 prod")]:
-        print(lab, [round((t[who * 16 + k] - base) / 1000, 2) if t[who * 16 + k] else None for k in range(7)])
+        print(lab, [round((t[who * 16 + k] - base) / 1000, 2) if t[who * 16 + k] else None for k in range(12)])
     print()

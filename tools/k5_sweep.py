@@ -49,7 +49,7 @@ def main():
             with torch.cuda.graph(g):
                 for _ in range(args.rep):
                     Z.sparse_decode_attn(shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, st.index, st.count,
-                                         st.out, st.workspace, index_phys=st.index_phys)
+                                         st.out, st.workspace)
             graphs.append(g)
         for g in graphs:
             g.replay()

@@ -431,29 +431,42 @@ static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][
     if (count > cap) set_status(status, ZOOMR_ERR_CAPACITY);
     *count_out = count < cap ? count : cap;
   }
-  for (int j = tid; j < sp && j < cap; j += blockDim.x) emit(j, j);  // sink
+  // Fill: thread t writes the contiguous output positions [t*E, (t+1)*E): one
+  // binary search for its first piece, then a walk that keeps the current piece
+  // in registers (shared memory is touched again only at a piece boundary).
+  // Output layout: [0, s') ++ pieces ++ [w0, T).
+  const int lim = count < cap ? count : cap;
+  const int E = (lim + (int)blockDim.x - 1) / (int)blockDim.x;
+  int j = tid * E;
+  const int j1 = min(lim, j + E);
   const int wbase = sp + total;
-  for (int j = tid; j < T - w0; j += blockDim.x)                      // window
-    if (wbase + j < cap) emit(wbase + j, w0 + j);
-  // one warp per piece; a warp's pieces are fetched into registers up front
-  // (lane u holds piece warp + u*nwarps) so the fill loop has no shared-memory
-  // round trip per piece
-  for (int i0w = warp; i0w < nt; i0w += 32 * nwarps) {
-    const int mine = i0w + lane * nwarps;
-    int ma = -1, mbase = 0, mlen = 0;
-    if (mine < nt) {
-      ma = piece[mine];
-      mbase = piece[nt + mine];
-      mlen = (mine + 1 < nt ? piece[nt + mine + 1] : total) - mbase;
+  const int *off = piece + nt;  // exclusive offsets of the clipped pieces
+  int i = 0;
+  if (nt > 0 && j < j1 && j < wbase && j1 > sp) {  // last piece with off <= max(j - sp, 0)
+    const int r = j > sp ? j - sp : 0;
+    int lo = 0, hi = nt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= r) lo = mid; else hi = mid - 1;
     }
-    const int np = min(32, (nt - i0w + nwarps - 1) / nwarps);
-    for (int u = 0; u < np; ++u) {
-      const int a = __shfl_sync(0xffffffffu, ma, u);
-      const int base = sp + __shfl_sync(0xffffffffu, mbase, u);
-      const int len = __shfl_sync(0xffffffffu, mlen, u);
-      if (a < 0) continue;
-      for (int j = lane; j < len; j += 32)
-        if (base + j < cap) emit(base + j, a + j);
+    i = lo;
+  }
+  int pc_start = nt ? piece[i] : 0, pc_off = nt ? off[i] : 0;
+  int pc_end = (i + 1 < nt) ? off[i + 1] : total;
+  for (; j < j1; ++j) {
+    if (j < sp) {
+      emit(j, j);  // sink
+    } else if (j < wbase) {
+      const int r = j - sp;
+      while (r >= pc_end) {  // next non-empty piece
+        ++i;
+        pc_start = piece[i];
+        pc_off = off[i];
+        pc_end = (i + 1 < nt) ? off[i + 1] : total;
+      }
+      emit(j, pc_start + (r - pc_off));
+    } else {
+      emit(j, w0 + (j - wbase));  // window
     }
   }
 }

@@ -99,3 +99,36 @@ def test_head_sharded_exchange_simulated(cfg_name, world):
         assert torch.equal(st.flags, full.flags) and torch.equal(st.count, full.count)
         assert torch.equal(st.index, full.index)
         torch.testing.assert_close(st.out, full.out[:, :, sh.q_start:sh.q_stop], atol=2e-6, rtol=0)
+
+
+@pytest.mark.parametrize("LR,c", [(64, 8), (1024, 32)])
+def test_stress_128k_sampled(LR, c):
+    """configs[4]: 128K context on the 8B shape (N_t = 1631 at L_R = 64: the vote-histogram
+    top-c path and a 10k+ entry index set; L_R = 1024: 33k+ token zoomed segments)."""
+    cfg = S.stress_config(LR, c)
+    inp = S.generate(cfg, device="cuda")
+    st = _run(inp, capacity=cfg.T)
+    rep = PY.check_sequence_sampled(inp, st, 0, {}, layers=[0, 17], qheads=[1, 30])
+    print(cfg.name, rep.get("index_counts"), rep.get("attn_max_abs_err"))
+    del st, inp
+    torch.cuda.empty_cache()
+
+
+def test_update_interval_holds_flags():
+    """U > 1 (reading Q11/Q14): between selection updates a4 re-derives the window from
+    the current T with the held flags; compare with the oracle's index for the held flags."""
+    cfg = S.CONFIGS["tiny"]
+    inp = S.generate(cfg, device="cuda", seed=3)
+    st = PY.make_step(inp)
+    PY.run_full(inp, st)
+    flags = st.flags.clone()
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    inp.seq_len.fill_(cfg.T - 7)  # an earlier step: the window slides back, flags are held
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st.run(inp.q, kv, seg, update_selection=False)
+    torch.cuda.synchronize()
+    assert torch.equal(st.flags, flags)
+    seg_h = PY.seg_host(inp, 0)
+    idx_ref = oracle.build_index(seg_h, flags[0, :len(seg_h)].cpu().numpy(), cfg.T - 7, cfg.sink, cfg.window)
+    cnt = int(st.count[0])
+    assert np.array_equal(st.index[0, :cnt].cpu().numpy(), idx_ref)

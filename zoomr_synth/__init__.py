@@ -92,6 +92,19 @@ def stress_config(LR: int, c: int, update_every: int = 1, grid_index: int = 0) -
                   update_every=update_every)
 
 
+def config_by_name(name: str) -> Config:
+    """'tiny' | '8b16k' | '8b32k' | '70b64k' | 'stress_LR<L_R>_c<c>_U<U>' (configs[4] grid point)."""
+    if name in CONFIGS:
+        return CONFIGS[name]
+    if name.startswith("stress"):
+        kv = {}
+        for part in name.split("_")[1:]:
+            key = part.rstrip("0123456789")
+            kv[key] = int(part[len(key):])
+        return stress_config(kv.get("LR", 64), kv.get("c", 8), kv.get("U", 1))
+    raise KeyError(name)
+
+
 @dataclass
 class Inputs:
     cfg: Config

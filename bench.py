@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--query", default="planted", choices=["planted", "diffuse"])
     ap.add_argument("--rotate", type=int, default=4, help="independent input sets cycled per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-early", action="store_true",
+                    help="A/B only: a5 waits for I_f before attending I_p / I_w")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -258,7 +260,7 @@ def run_ours(args):
     sets = []
     for r in range(R):
         inp = S.generate(cfg, device="cuda", seed=cfg.seed + 1000 * rank + 17 * r, query_mode=args.query)
-        st = ZoomrStep(shape, inp.q.shape[0], inp.bounds.shape[1], cfg.T, prm)
+        st = ZoomrStep(shape, inp.q.shape[0], inp.bounds.shape[1], cfg.T, prm, early_known=not args.no_early)
         kv = (inp.k_pool, inp.v_pool, inp.page_table)
         seg = (inp.bounds, inp.num_summaries, inp.seq_len)
         st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))  # initial cache (untimed)
@@ -272,8 +274,7 @@ def run_ours(args):
         phys = st.index_phys if st.use_phys else None
         ga = torch.cuda.CUDAGraph()
         with torch.cuda.graph(ga):
-            Z.sparse_decode_attn(shape, inp.q, inp.k_pool, inp.v_pool, inp.page_table, st.index, st.count,
-                                 st.out, st.workspace, dev_status=st.status, index_phys=phys)
+            st.attend(inp.q, kv, inp.seq_len)
         g.replay()  # leave the full selection's flags / index in place
         sets.append(dict(inp=inp, st=st, g=g, gl=gl, ga=ga, kv=kv, seg=seg, newest=newest, phys=phys))
     torch.cuda.synchronize()

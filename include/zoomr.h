@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 1
+#define ZOOMR_ABI_VERSION 2
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -166,10 +166,21 @@ size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
  * as written by a4 (count >= 1).  index_phys (nullable, [B][index_capacity]):
  * the page-resolved rows zoomr_select_fused can write alongside I_f
  * (page_table[t/P]*H_kv*P + t%P); when given, the page table is not read.
- * softmax_scale is normally 1/sqrt(d). */
+ * softmax_scale is normally 1/sqrt(d).
+ *
+ * seq_len (nullable, int32 [B], device) + sink + window: when given, I_f MUST
+ * be a4's output for the same T = seq_len[b], sink and window, i.e. start with
+ * I_p = [0, min(sink, T)) and end with I_w = [max(min(sink, T), T - window), T)
+ * (readings Q12, Q13, Q17).  The kernel then attends over those rows -- known
+ * from T alone -- before it waits for the producer of I_f (it is launched with
+ * programmatic dependent launch), so that part of the gather overlaps the
+ * selection; the rest of I_f is read from `index` afterwards.  Only this
+ * kernel's workspace is written before the wait.  NULL: every row comes from
+ * `index` (any sorted or unsorted list of positions is then accepted). */
 int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
                              const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                              const int32_t *index_count, int32_t index_capacity,
+                             const int32_t *seq_len, int32_t sink, int32_t window,
                              float softmax_scale, float *out, void *workspace,
                              size_t workspace_bytes, int32_t *dev_status, void *stream);
 

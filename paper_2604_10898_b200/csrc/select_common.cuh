@@ -139,21 +139,30 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
   for (int x = threadIdx.x; x < G * D; x += blockDim.x) qs[x] = __bfloat162float(qb[x]);
   __syncthreads();
   constexpr int FPL = D / 8;  // floats per octet lane
+  constexpr int NV = FPL >= 4 ? FPL / 4 : 1;
   const int oct = lane >> 3, l8 = lane & 7;
-  for (int base = warp * 8; base < nt; base += nw * 8) {
-    float4 kv[2][FPL >= 4 ? FPL / 4 : 1];
-    float2 kv2[2];
+  // each warp takes 8 rows per step (2 per octet); the next step's rows are
+  // loaded before this step's math (double buffering), so at large N_t the
+  // loop streams instead of paying one round trip per step
+  float4 kv[2][NV], kn[2][NV];
+  float2 kv2[2], kn2[2];
+  auto load = [&](int base, float4 (&dst)[2][NV], float2 (&dst2)[2]) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int i = base + u * 4 + oct;
       const float *row = mk + (int64_t)(i < nt ? i : 0) * D;
       if constexpr (FPL >= 4) {
 #pragma unroll
-        for (int m = 0; m < FPL / 4; ++m) kv[u][m] = *reinterpret_cast<const float4 *>(row + m * 32 + l8 * 4);
+        for (int m = 0; m < NV; ++m) dst[u][m] = *reinterpret_cast<const float4 *>(row + m * 32 + l8 * 4);
       } else {
-        kv2[u] = *reinterpret_cast<const float2 *>(row + l8 * 2);
+        dst2[u] = *reinterpret_cast<const float2 *>(row + l8 * 2);
       }
     }
+  };
+  const int step = nw * 8;
+  if (warp * 8 < nt) load(warp * 8, kv, kv2);
+  for (int base = warp * 8; base < nt; base += step) {
+    if (base + step < nt) load(base + step, kn, kn2);
     float acc[2][G];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
@@ -162,7 +171,7 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
         float a = 0.f;
         if constexpr (FPL >= 4) {
 #pragma unroll
-          for (int m = 0; m < FPL / 4; ++m) {
+          for (int m = 0; m < NV; ++m) {
             const float4 qv = *reinterpret_cast<const float4 *>(qs + hh * D + m * 32 + l8 * 4);
             a = fmaf(kv[u][m].x, qv.x, a);
             a = fmaf(kv[u][m].y, qv.y, a);
@@ -190,6 +199,12 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
             if (alpha_out) alpha_out[hh * ald_out + i] = acc[u][hh];
           }
       }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int m = 0; m < NV; ++m) kv[u][m] = kn[u][m];
+      kv2[u] = kn2[u];
     }
   }
   __syncthreads();
@@ -396,7 +411,7 @@ static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][
       phys[j] = pt[lp] * HkvP + (t - lp * P);
     }
   };
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int tid = threadIdx.x;
   const int sp = sink < T ? sink : T;                  // s'
   const int w0 = (T - window > sp) ? T - window : sp;  // start of the window piece
   const int per = (nt + (int)blockDim.x - 1) / (int)blockDim.x;

@@ -85,11 +85,13 @@ struct AttnParams {
   const int32_t *count;
   int32_t cap;
   float *out;
-  float *ws_part;  // [NW][2][G*(D+2)]
+  float *ws_part;  // [2][NW + B*L*Hkv][SLOT]: partial of (phase, warp w, segment s) at [phase][w + s]
   int32_t *ws_cnt; // [B*L*Hkv]
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
   int32_t pt_smem;               // page table staged in shared memory (B*max_pages <= kPtSmem)
   float scale_log2;
+  const int32_t *seq_len;  // nullable: with it, I_p and I_w are attended before the wait (phase A)
+  int32_t sink, window;
   int32_t *status;
 };
 
@@ -165,7 +167,14 @@ struct Sched {
   int64_t NWe;  // effective number of math warps (<= T_tot)
   int32_t B, LH;  // LH = L * Hkv segments per sequence
   __device__ __forceinline__ int64_t range_start(int64_t w) const { return T_tot * w / NWe; }
-  __device__ __forceinline__ int64_t warp_of(int64_t t) const { return ((t + 1) * NWe - 1) / T_tot; }
+  double inv_T;   // 1 / T_tot (warp_of without a 64-bit division)
+  __device__ __forceinline__ int64_t warp_of(int64_t t) const {  // floor(((t + 1) * NWe - 1) / T_tot)
+    const int64_t x = (t + 1) * NWe - 1;
+    int64_t q = (int64_t)((double)x * inv_T);  // x < 2^53: off by at most one
+    if (q * T_tot > x) --q;
+    else if ((q + 1) * T_tot <= x) ++q;
+    return q;
+  }
   // global tile -> (b, segment within b, tile within segment, tiles per segment of b)
   __device__ __forceinline__ void locate(int64_t t, int &b, int &seg, int &tis, int &nts) const {
     int lo = 0, hi = B - 1;
@@ -181,6 +190,16 @@ struct Sched {
   }
 };
 
+// Two phases of work per launch.  Phase A: the rows of I_f that are known from
+// T alone -- I_p = [0, s') and I_w = [w0, T), which a4 puts first and last in
+// I_f (readings Q12, Q13, Q17) -- are attended BEFORE griddepcontrol.wait, so
+// that part of the gather overlaps the tail of the kernel that builds I_f.
+// Phase B: the middle of I_f (zoomed segments and kept summaries), positions
+// [s', s' + n_B) of `index`, after the wait.  Each phase is its own stream-K
+// split over all math warps; a segment's softmax partials from both phases are
+// merged by the last-arriving warp.  Phase-A partials are published before the
+// wait but counted (arrival atomics) only after it, when the phase-B split --
+// and so the number of parts of every segment -- is known.
 template <int D, int G>
 __global__ void __launch_bounds__(64 * kPairs, 1)
     sparse_attn_kernel(const AttnParams p, const __grid_constant__ TmaMaps maps) {
@@ -190,37 +209,53 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   unsigned char *smem = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES);  // [kPairs][kStages]
   uint64_t *empty = full + kPairs * kStages;                             // [kPairs][kStages]
-  int32_t *pts = reinterpret_cast<int32_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // [kPtSmem] page tables
-  int32_t *prefix = pts + (p.pt_smem ? kPtSmem : 0);                                  // [B+1]
-  int32_t *cnts = prefix + p.B + 1;                                                   // [B] clamped |I_f|
+  uint64_t *bready = reinterpret_cast<uint64_t *>(smem + S::RING_BYTES + S::BAR_BYTES);  // phase-B schedule published
+  int4 *info = reinterpret_cast<int4 *>(bready + 2);  // [B]: a1, T - a2, n_A, n_B
+  int32_t *pts = reinterpret_cast<int32_t *>(info + p.B);  // [kPtSmem] page tables
+  int32_t *prefA = pts + (p.pt_smem ? kPtSmem : 0);        // [B+1] first phase-A tile of sequence b
+  int32_t *prefB = prefA + p.B + 1;                        // [B+1] first phase-B tile
+  int32_t *bstate = prefB + p.B + 1;                       // phase-B schedule: 0 unclaimed, 1 claimed
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
+  const int LH = p.L * p.Hkv;
 
   if (threadIdx.x == 0) {
     for (int x = 0; x < kPairs * kStages; ++x) {
       mbar_init(&full[x], 33);  // producer lane 0's expect_tx arrive + one cp.async (noinc) arrive per lane
       mbar_init(&empty[x], 1);  // the math warp's lane 0
     }
+    *bstate = 0;
+    mbar_init(bready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // The page tables are inputs, not outputs of the preceding kernel (a4 / the
-  // fused select): stage them while that kernel is still finishing.
+  // Page tables, T, q and the pools are inputs, not outputs of the preceding
+  // kernel (a4 / the fused select): read them while that kernel is finishing.
   if (p.pt_smem)
     for (int x = threadIdx.x; x < p.B * p.max_pages; x += blockDim.x) pts[x] = p.page_table[x];
-  // Programmatic dependent launch: everything above overlaps the producer of
-  // I_f (a4 / the fused select); from here on its results are visible.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // tiles per sequence -> prefix (warp 0 scans in chunks of 32 sequences)
-  if (warp == 0) {
+  if (warp == 0) {  // phase-A tiles per sequence -> prefix (chunks of 32 sequences)
     int carry = 0;
     for (int b0 = 0; b0 < p.B; b0 += 32) {
       const int b = b0 + lane;
       int n = 0;
       if (b < p.B) {
-        int c = p.count[b];
-        c = c < p.cap ? c : p.cap;
-        cnts[b] = c;
-        n = c > 0 ? (c + kTile - 1) / kTile * p.L * p.Hkv : 0;
+        // phase A = the first a1 and the last a2 entries of I_f: the sink and the
+        // newest window rows, n_A = a1 + a2 rounded DOWN to whole tiles (the
+        // window rows left over join phase B, whose index positions stay
+        // contiguous: [a1, |I_f| - a2)), so neither phase adds a ragged tile
+        int a1 = 0, a2 = 0;
+        if (p.seq_len) {
+          const int T = max(p.seq_len[b], 0);
+          const int sp = min(p.sink, T);
+          const int w0 = max(sp, T - p.window);
+          const int na = (sp + (T - w0)) / kTile * kTile;
+          a1 = min(sp, na);
+          a2 = na - a1;
+          info[b] = make_int4(a1, T - a2, na, 0);
+        } else {
+          info[b] = make_int4(0, 0, 0, 0);
+        }
+        const int na = a1 + a2;
+        n = na > 0 ? (na + kTile - 1) / kTile * LH : 0;
       }
       int incl = n;
 #pragma unroll
@@ -228,57 +263,143 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      if (b < p.B) prefix[b] = carry + incl - n;
+      if (b < p.B) prefA[b] = carry + incl - n;
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) prefix[p.B] = carry;
+    if (lane == 0) prefA[p.B] = carry;
   }
   __syncthreads();
 
-  Sched sc;
-  sc.prefix = prefix;
-  sc.T_tot = prefix[p.B];
-  sc.B = p.B;
-  sc.LH = p.L * p.Hkv;
-  if (sc.T_tot == 0) return;
   const int64_t NW = (int64_t)gridDim.x * kPairs;
-  sc.NWe = NW < sc.T_tot ? NW : sc.T_tot;
-
   const int pair = warp % kPairs;
   const bool producer = warp >= kPairs;
   const int64_t gw = (int64_t)blockIdx.x * kPairs + pair;  // global math-warp id of the pair
-  if (gw >= sc.NWe) return;
-  const int64_t r0 = sc.range_start(gw), r1 = sc.range_start(gw + 1);
-  const int64_t ntiles = r1 - r0;
+  Sched sA, sB;
+  sA.prefix = prefA;
+  sA.T_tot = prefA[p.B];
+  sA.NWe = NW < sA.T_tot ? NW : sA.T_tot;
+  sA.inv_T = sA.T_tot > 0 ? 1.0 / (double)sA.T_tot : 0.0;
+  sA.B = sB.B = p.B;
+  sA.LH = sB.LH = LH;
+  sB.prefix = prefB;
+  sB.T_tot = 0;
+  sB.NWe = 0;
+  int64_t a0 = 0, nAk = 0, b0r = 0, nBk = 0;  // this warp's tiles: [a0, a0+nAk) of A, [b0r, b0r+nBk) of B
+  if (gw < sA.NWe) {
+    a0 = sA.range_start(gw);
+    nAk = sA.range_start(gw + 1) - a0;
+  }
+  bool bres = false;  // phase-B schedule known (implies griddepcontrol.wait done)
+  // Programmatic dependent launch: after the wait the producer of I_f has
+  // completed and its writes are visible.  The first warp to get here derives
+  // n_B and the phase-B prefix for the CTA; the others wait for it.
+  auto resolve_b = [&]() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int st = 0;
+    if (lane == 0) st = atomicCAS(bstate, 0, 1);
+    st = __shfl_sync(0xffffffffu, st, 0);
+    if (st == 0) {
+      int carry = 0;
+      for (int c0 = 0; c0 < p.B; c0 += 32) {
+        const int b = c0 + lane;
+        int n = 0;
+        if (b < p.B) {
+          int c = p.count[b];
+          c = c < p.cap ? c : p.cap;
+          const int nb = max(0, c - info[b].z);
+          info[b].w = nb;
+          n = nb > 0 ? (nb + kTile - 1) / kTile * LH : 0;
+        }
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (b < p.B) prefB[b] = carry + incl - n;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) prefB[p.B] = carry;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bready);  // release: the schedule above is visible to the waiters
+    } else {
+      mbar_wait(bready, 0);  // acquire (suspends instead of hammering shared memory)
+    }
+    __syncwarp();
+    sB.T_tot = prefB[p.B];
+    sB.NWe = NW < sB.T_tot ? NW : sB.T_tot;
+    sB.inv_T = sB.T_tot > 0 ? 1.0 / (double)sB.T_tot : 0.0;
+    if (gw < sB.NWe) {
+      b0r = sB.range_start(gw);
+      nBk = sB.range_start(gw + 1) - b0r;
+    }
+    bres = true;
+  };
+  // k-th tile of this warp's list (A tiles, then B tiles) -> (phase, b, segment,
+  // tile in segment).  Tiles are visited in order, so the walk advances
+  // incrementally; it searches the prefix only at its start and at the phase switch.
+  struct Walk {
+    int ph = -1, b = 0, seg = 0, tis = 0, nts = 0;
+    int64_t k = -2;
+  };
+  auto where = [&](Walk &w, int64_t k) {
+    const int ph = k < nAk ? 0 : 1;
+    if (ph == w.ph && k == w.k + 1) {
+      w.k = k;
+      if (++w.tis < w.nts) return;
+      w.tis = 0;
+      if (++w.seg < LH) return;
+      w.seg = 0;
+      const int32_t *pf = ph ? prefB : prefA;
+      do {
+        ++w.b;
+      } while (w.b < p.B - 1 && pf[w.b + 1] == pf[w.b]);  // sequences without tiles in this phase
+      w.nts = (pf[w.b + 1] - pf[w.b]) / LH;
+      return;
+    }
+    w.ph = ph;
+    w.k = k;
+    if (ph == 0) sA.locate(a0 + k, w.b, w.seg, w.tis, w.nts);
+    else sB.locate(b0r + (k - nAk), w.b, w.seg, w.tis, w.nts);
+  };
   const uint32_t ring = smem_u32(smem) + (uint32_t)(pair * kStages * S::STAGE_BYTES);
   uint64_t *fullp = full + pair * kStages;
   uint64_t *emptyp = empty + pair * kStages;
 
   if (producer) {
-    // ================= producer: 3-stage address pipeline, LDGSTS copies =====
-    // A(k+2): I_f position load   B(k+1): page-table load   C(k): row copies.
-    // Each dependent load is consumed one iteration after it is issued, so the
+    // ================= producer: address pipeline + TMA / cp.async copies =====
+    // A(k+4): I_f position   B(k+2): page-table entry   C(k): row copies.
+    // Each dependent load is consumed two iterations after it is issued, so the
     // index -> page -> row chain never stalls the copy issue in steady state.
     struct Addr {
-      int b, l, g, ok, tok, slot, page;
+      int ph, b, l, g, ok, tok, slot, page;
     };
+    Walk wk;
     auto stage_a = [&](int64_t k, Addr &a) {
-      int seg, tis, nts;
-      sc.locate(r0 + k, a.b, seg, tis, nts);
-      const int cnt = cnts[a.b];
+      where(wk, k);
+      a.ph = wk.ph;
+      a.b = wk.b;
+      const int seg = wk.seg, tis = wk.tis;
+      const int4 in = info[a.b];
       a.l = seg / p.Hkv;
       a.g = seg - a.l * p.Hkv;
       const int pos = tis * kTile + lane;
-      a.ok = pos < cnt;
-      // with index_phys, `tok` carries the page-resolved row and stage B is a no-op;
-      // the load is guarded by the capacity, not the count, so it does not wait for it
-      const int32_t *src = p.index_phys ? p.index_phys : p.index;
-      a.tok = pos < p.cap ? src[(int64_t)a.b * p.cap + pos] : 0;
+      if (a.ph == 0) {  // [0, s') ++ [w0, T)
+        a.ok = pos < in.z;
+        a.tok = pos < in.x ? pos : in.y + (pos - in.x);
+      } else {
+        a.ok = pos < in.w;
+        // with index_phys, `tok` carries the page-resolved row and stage B is a no-op;
+        // the load is guarded by the capacity, not the count, so it does not wait for it
+        const int ip = in.x + pos;
+        const int32_t *src = p.index_phys ? p.index_phys : p.index;
+        a.tok = ip < p.cap ? src[(int64_t)a.b * p.cap + ip] : 0;
+      }
     };
     auto stage_b = [&](Addr &a) {
       a.page = 0;
       a.slot = 0;
-      if (a.ok && !p.index_phys) {
+      if (a.ok && !(a.ph && p.index_phys)) {
         const int lp = p.Pshift >= 0 ? (a.tok >> p.Pshift) : a.tok / p.P;
         a.slot = a.tok - lp * p.P;
         if (a.tok >= 0 && lp < p.max_pages)
@@ -290,10 +411,14 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     // kAheadB tiles ahead of the copies
     constexpr int kAheadA = 4, kAheadB = 2;
     Addr q0{}, q1{}, q2{}, q3{}, q4{};  // tiles k .. k+4
-    const int rsub = lane / S::CPR, ch = lane % S::CPR;
+    int64_t ntiles = nAk;
     // one loop, one call site per stage (the pipeline fill is its first kAheadA
     // iterations): the kernel's code stays small enough for the instruction cache
     for (int64_t k = -kAheadA; k < ntiles; ++k) {
+      if (!bres && k + kAheadA >= nAk) {  // first phase-B tile enters the pipeline
+        resolve_b();
+        ntiles = nAk + nBk;
+      }
       if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
       if (k + kAheadB >= 0 && k + kAheadB < ntiles) stage_b(q2);
       if (k < 0) {
@@ -306,9 +431,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       Addr &ac = q0;
       // stage C: global row of every token of tile k
       const int cok = ac.ok;
+      const bool usephys = ac.ph && p.index_phys;
       int64_t grow = 0;
       int page = ac.page;
-      if (p.index_phys) {
+      if (usephys) {
         // row(l, g, t) = (l*num_pages*H_kv + g)*P + phys(t); consecutive phys = contiguous rows
         int phys = ac.tok;
         if (cok && (phys < 0 || (int64_t)phys >= p.num_pages * p.Hkv * p.P)) {
@@ -327,7 +453,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       const int ptok = __shfl_up_sync(0xffffffffu, ac.tok, 1);
       const int ppage = __shfl_up_sync(0xffffffffu, page, 1);
       const int pok = __shfl_up_sync(0xffffffffu, cok, 1);
-      const bool cont = cok && lane > 0 && pok && ptok + 1 == ac.tok && (p.index_phys || ppage == page);
+      const bool cont = cok && lane > 0 && pok && ptok + 1 == ac.tok && (usephys || ppage == page);
       const unsigned validm = __ballot_sync(0xffffffffu, cok);
       const unsigned startm = __ballot_sync(0xffffffffu, cok && !cont);
       const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
@@ -402,13 +528,44 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   constexpr int HDR = (2 * G + 3) / 4 * 4;  // m[G], l[G] padded to a 16-byte boundary
   constexpr int SLOT = HDR + G * D;         // partial result: header, then O[G][D]
 
-  int first_b = -1, first_seg = -1;  // the first segment of this warp's range (slot rule)
-  int cur_b = -1, cur_seg = -1;
+  int cur_ph = -2, cur_b = -1, cur_seg = -1;  // -2: no segment yet (never equal to a past-the-end k)
+  int npend = 0;  // phase-A partials published before the wait, not yet counted: the first npend segments of the A range
   uint32_t qf[NKS][2];
   float o[NKS][4], o2[kTwoN ? NKS : 1][4];
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-  auto flush = [&](int b, int seg) {
+  // parts of segment (b, seg): A warps [wf0, wf0 + n0w), B warps [wf1, wf1 + n1w) (needs bres)
+  auto seg_parts = [&](int b, int seg, int64_t &wf0, int &n0w, int64_t &wf1, int &n1w) {
+    n0w = n1w = 0;
+    wf0 = wf1 = 0;
+    const int na = (prefA[b + 1] - prefA[b]) / LH;
+    if (na > 0) {
+      const int64_t st0 = prefA[b] + (int64_t)seg * na;
+      wf0 = sA.warp_of(st0);
+      n0w = (int)(sA.warp_of(st0 + na - 1) - wf0 + 1);
+    }
+    const int nb = (prefB[b + 1] - prefB[b]) / LH;
+    if (nb > 0) {
+      const int64_t st0 = prefB[b] + (int64_t)seg * nb;
+      wf1 = sB.warp_of(st0);
+      n1w = (int)(sB.warp_of(st0 + nb - 1) - wf1 + 1);
+    }
+  };
+  // Partial-result slot of (phase, warp w, segment s): the (w, s) pairs a
+  // stream-K split produces form a staircase on which w + s strictly increases,
+  // so w + s (< NW + #segments) is a unique slot per phase.
+  const int64_t nslots = NW + (int64_t)p.B * LH;
+  auto part_slot = [&](int ph, int64_t w, int b, int seg) -> int64_t {
+    return ph * nslots + w + (int64_t)b * LH + seg;
+  };
+  // where part j of segment (b, seg) lives
+  auto part_ptr = [&](int b, int seg, int j, int64_t wf0, int n0w, int64_t wf1) -> const float * {
+    const int ph = j < n0w ? 0 : 1;
+    const int64_t w = ph ? wf1 + (j - n0w) : wf0 + j;
+    return p.ws_part + part_slot(ph, w, b, seg) * SLOT;
+  };
+
+  auto flush = [&](int ph, int b, int seg) {
     // finish the segment's softmax state and publish it (final or partial)
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -436,215 +593,187 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     // owners: threads whose columns are the hi copies of real heads
     const bool owner = (G == 8) || (G == 4 && tq < 2) || (G <= 2 && tq == 0);
     const int nh = (G == 1) ? 1 : 2;  // heads held by an owner thread: n0 (and n0+1)
-    const int l = seg / p.Hkv, g = seg - l * p.Hkv;
-    const int nts = (sc.prefix[b + 1] - sc.prefix[b]) / sc.LH;
-    const int64_t st0 = sc.prefix[b] + (int64_t)seg * nts, st1 = st0 + nts;
-    const int64_t wf = sc.warp_of(st0), wl = sc.warp_of(st1 - 1);
-    float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
-    if (wf == wl) {  // this warp owns the whole segment: final output
+    int64_t wf0, wf1;
+    int n0w, n1w;
+    if (bres) {
+      seg_parts(b, seg, wf0, n0w, wf1, n1w);
+      if (n0w + n1w == 1) {  // this warp is the segment's only part: final output
+        const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+        float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
+        if (owner) {
+          const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+#pragma unroll
+          for (int me = 0; me < NKS; ++me) {
+            const int e = me * 16 + gq;
+            ob[(int64_t)n0 * D + e] = ov[me][0] * inv0;
+            ob[(int64_t)n0 * D + e + 8] = ov[me][2] * inv0;
+            if (nh == 2) {
+              ob[(int64_t)(n0 + 1) * D + e] = ov[me][1] * inv1;
+              ob[(int64_t)(n0 + 1) * D + e + 8] = ov[me][3] * inv1;
+            }
+          }
+        }
+        return;
+      }
+    }
+    {  // partial
+      float *ps = p.ws_part + part_slot(ph, gw, b, seg) * SLOT;
       if (owner) {
-        const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+        if (gq == 0) {
+          ps[n0] = m0;
+          ps[G + n0] = l0;
+          if (nh == 2) {
+            ps[n0 + 1] = m1;
+            ps[G + n0 + 1] = l1;
+          }
+        }
 #pragma unroll
         for (int me = 0; me < NKS; ++me) {
           const int e = me * 16 + gq;
-          ob[(int64_t)n0 * D + e] = ov[me][0] * inv0;
-          ob[(int64_t)n0 * D + e + 8] = ov[me][2] * inv0;
+          ps[HDR + n0 * D + e] = ov[me][0];
+          ps[HDR + n0 * D + e + 8] = ov[me][2];
           if (nh == 2) {
-            ob[(int64_t)(n0 + 1) * D + e] = ov[me][1] * inv1;
-            ob[(int64_t)(n0 + 1) * D + e + 8] = ov[me][3] * inv1;
+            ps[HDR + (n0 + 1) * D + e] = ov[me][1];
+            ps[HDR + (n0 + 1) * D + e + 8] = ov[me][3];
           }
         }
       }
+      __syncwarp();  // orders the lanes' partial stores before lane 0's release
+    }
+    if (!bres) {  // phase A before the wait: count it later
+      ++npend;
       return;
     }
-    // partial: slot 0 if this is the warp's first segment, else slot 1
-    const int slot = (b == first_b && seg == first_seg) ? 0 : 1;
-    float *ps = p.ws_part + ((int64_t)gw * 2 + slot) * SLOT;
-    if (owner) {
-      if (gq == 0) {
-        ps[n0] = m0;
-        ps[G + n0] = l0;
-        if (nh == 2) {
-          ps[n0 + 1] = m1;
-          ps[G + n0 + 1] = l1;
-        }
+    // count the pending phase-A partials (segments of the A range in order), then
+    // this one; the last arriving part of a segment merges all of its parts
+    int64_t t = a0;
+    const int narr = npend + 1;
+    npend = 0;
+    for (int it = 0; it < narr; ++it) {
+      int xb = b, xs = seg;
+      if (it + 1 < narr) {
+        int xt, xn;
+        sA.locate(t, xb, xs, xt, xn);
+        t += xn - xt;  // first tile of the next segment
       }
-#pragma unroll
-      for (int me = 0; me < NKS; ++me) {
-        const int e = me * 16 + gq;
-        ps[HDR + n0 * D + e] = ov[me][0];
-        ps[HDR + n0 * D + e + 8] = ov[me][2];
-        if (nh == 2) {
-          ps[HDR + (n0 + 1) * D + e] = ov[me][1];
-          ps[HDR + (n0 + 1) * D + e + 8] = ov[me][3];
-        }
-      }
-    }
-    __syncwarp();  // orders the lanes' partial stores before lane 0's release
-    int32_t *cnt = p.ws_cnt + (int64_t)b * sc.LH + seg;
-    int old = 0;
-    if (lane == 0)
-      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != (int)(wl - wf)) return;  // not the last arriving warp
-    __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
-    // last arriver: merge the partials of warps wf..wl (fixed order -> deterministic).
-    const int nparts = (int)(wl - wf + 1);
-    constexpr int NV4 = G * D / 4;
-    constexpr int PER = (NV4 + 31) / 32;
-    constexpr int NPF = G >= 8 ? 2 : 4;  // fast path: every load of up to NPF parts in flight at once
-    if (nparts <= NPF) {
-      const float *qp[NPF];
-      float mh[NPF][G], lh[NPF][G];
-      float4 ov4[NPF][PER];
-#pragma unroll
-      for (int j = 0; j < NPF; ++j) {
-        if (j < nparts) {
-          int fb, fs, ft, fn;
-          sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
-          qp[j] = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
-#pragma unroll
-          for (int h = 0; h < G; ++h) {
-            mh[j][h] = __ldcg(qp[j] + h);
-            lh[j][h] = __ldcg(qp[j] + G + h);
-          }
-#pragma unroll
-          for (int u = 0; u < PER; ++u) {
-            const int f = lane + 32 * u;
-            ov4[j][u] = f < NV4 ? __ldcg(reinterpret_cast<const float4 *>(qp[j] + HDR) + f) : make_float4(0, 0, 0, 0);
-          }
-        }
-      }
+      seg_parts(xb, xs, wf0, n0w, wf1, n1w);
+      const int nparts = n0w + n1w;
+      int32_t *cnt = p.ws_cnt + (int64_t)xb * LH + xs;
+      int old = 0;
+      if (lane == 0)
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old != nparts - 1) continue;  // not the last arriving part
+      __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
+      // last arriver: online merge of the parts in a fixed order (deterministic),
+      // NPF parts per round with all their loads in flight
+      const int xl = xs / p.Hkv, xg = xs - xl * p.Hkv;
+      float *ob = p.out + (((int64_t)xb * p.L + xl) * Hq + (int64_t)xg * G) * D;
+      constexpr int NV4 = G * D / 4;
+      constexpr int PER = (NV4 + 31) / 32;
+      constexpr int NPF = G >= 8 ? 2 : 4;
       float Mh[G], Lh[G];
+      float4 acc[PER];
 #pragma unroll
       for (int h = 0; h < G; ++h) {
         Mh[h] = -INFINITY;
         Lh[h] = 0.f;
-#pragma unroll
-        for (int j = 0; j < NPF; ++j)
-          if (j < nparts) Mh[h] = fmaxf(Mh[h], mh[j][h]);
       }
-      float w[NPF][G];
 #pragma unroll
-      for (int j = 0; j < NPF; ++j)
+      for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j0 = 0; j0 < nparts; j0 += NPF) {
+        float mh[NPF][G], lh[NPF][G];
+        float4 ov4[NPF][PER];
+#pragma unroll
+        for (int j = 0; j < NPF; ++j) {
+          if (j0 + j < nparts) {
+            const float *qp = part_ptr(xb, xs, j0 + j, wf0, n0w, wf1);
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              mh[j][h] = __ldcg(qp + h);
+              lh[j][h] = __ldcg(qp + G + h);
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+              const int f = lane + 32 * u;
+              ov4[j][u] = f < NV4 ? __ldcg(reinterpret_cast<const float4 *>(qp + HDR) + f)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              mh[j][h] = -INFINITY;
+              lh[j][h] = 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) ov4[j][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        float w[NPF][G], so[G];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          w[j][h] = j < nparts ? ex2(mh[j][h] - Mh[h]) : 0.f;
-          Lh[h] += j < nparts ? lh[j][h] * w[j][h] : 0.f;
+          float mn = Mh[h];
+#pragma unroll
+          for (int j = 0; j < NPF; ++j) mn = fmaxf(mn, mh[j][h]);
+          so[h] = ex2(Mh[h] - mn);  // -inf -> 0 on the first round
+          Lh[h] *= so[h];
+#pragma unroll
+          for (int j = 0; j < NPF; ++j) {
+            w[j][h] = ex2(mh[j][h] - mn);
+            Lh[h] += lh[j][h] * w[j][h];
+          }
+          Mh[h] = mn;
         }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int h = (4 * (lane + 32 * u)) / D < G ? (4 * (lane + 32 * u)) / D : G - 1;
+          float4 a = acc[u];
+          a.x *= so[h];
+          a.y *= so[h];
+          a.z *= so[h];
+          a.w *= so[h];
+#pragma unroll
+          for (int j = 0; j < NPF; ++j) {
+            a.x += ov4[j][u].x * w[j][h];
+            a.y += ov4[j][u].y * w[j][h];
+            a.z += ov4[j][u].z * w[j][h];
+            a.w += ov4[j][u].w * w[j][h];
+          }
+          acc[u] = a;
+        }
+      }
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const int f = lane + 32 * u;
         if (f < NV4) {
-          const int h = (4 * f) / D;
-          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int j = 0; j < NPF; ++j)
-            if (j < nparts) {
-              a.x += ov4[j][u].x * w[j][h];
-              a.y += ov4[j][u].y * w[j][h];
-              a.z += ov4[j][u].z * w[j][h];
-              a.w += ov4[j][u].w * w[j][h];
-            }
-          const float inv = 1.f / Lh[h];
-          reinterpret_cast<float4 *>(ob)[f] = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+          const float inv = 1.f / Lh[(4 * f) / D];
+          reinterpret_cast<float4 *>(ob)[f] =
+              make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
         }
       }
       if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
-      return;
     }
-    // (general path) lane j fetches part j's header (slot pointer, m[G], l[G])
-    // so that all the round trips of a chunk of 32 parts are in flight together.
-    float Mh[G], Lh[G];
-    float4 acc[PER];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      Mh[h] = -INFINITY;
-      Lh[h] = 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int j0 = 0; j0 < nparts; j0 += 32) {
-        const int j = j0 + lane;
-        const float *q2 = nullptr;
-        float mj[G], lj[G];
-        if (j < nparts) {
-          int fb, fs, ft, fn;
-          sc.locate(sc.range_start(wf + j), fb, fs, ft, fn);
-          q2 = p.ws_part + ((wf + j) * 2 + ((fb == b && fs == seg) ? 0 : 1)) * SLOT;
-#pragma unroll
-          for (int h = 0; h < G; ++h) {
-            mj[h] = __ldcg(q2 + h);
-            lj[h] = __ldcg(q2 + G + h);
-          }
-        }
-        if (pass == 0) {  // per-head max over all parts
-          if (j < nparts)
-#pragma unroll
-            for (int h = 0; h < G; ++h) Mh[h] = fmaxf(Mh[h], mj[h]);
-          continue;
-        }
-        float wj[G];
-#pragma unroll
-        for (int h = 0; h < G; ++h) {
-          wj[h] = j < nparts ? ex2(mj[h] - Mh[h]) : 0.f;
-          Lh[h] += j < nparts ? lj[h] * wj[h] : 0.f;
-        }
-        const int nj = min(32, nparts - j0);
-        for (int u0 = 0; u0 < nj; ++u0) {
-          const float *qq = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)q2, u0);
-          float w[G];
-#pragma unroll
-          for (int h = 0; h < G; ++h) w[h] = __shfl_sync(0xffffffffu, wj[h], u0);
-          const float4 *O4 = reinterpret_cast<const float4 *>(qq + HDR);
-#pragma unroll
-          for (int u = 0; u < PER; ++u) {
-            const int f = lane + 32 * u;
-            if (f < NV4) {
-              const float4 v = __ldcg(O4 + f);
-              const float ww = w[(4 * f) / D];
-              acc[u].x += v.x * ww;
-              acc[u].y += v.y * ww;
-              acc[u].z += v.z * ww;
-              acc[u].w += v.w * ww;
-            }
-          }
-        }
-      }
-      if (pass == 0) {
-#pragma unroll
-        for (int h = 0; h < G; ++h)
-#pragma unroll
-          for (int off = 16; off; off >>= 1) Mh[h] = fmaxf(Mh[h], __shfl_xor_sync(0xffffffffu, Mh[h], off));
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < G; ++h)
-#pragma unroll
-      for (int off = 16; off; off >>= 1) Lh[h] += __shfl_xor_sync(0xffffffffu, Lh[h], off);
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int f = lane + 32 * u;
-      if (f < NV4) {
-        const float inv = 1.f / Lh[(4 * f) / D];
-        reinterpret_cast<float4 *>(ob)[f] =
-            make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
-      }
-    }
-    if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
   };
 
-  for (int64_t k = 0; k <= ntiles; ++k) {  // k == ntiles: only the final flush
-    int b = -1, seg = -1, tis = 0, nts = 0;
-    if (k < ntiles) sc.locate(r0 + k, b, seg, tis, nts);
-    if (k == 0) {
-      first_b = b;
-      first_seg = seg;
+  Walk wk;
+  int64_t ntot = nAk;
+  for (int64_t k = 0;; ++k) {  // the iteration past the last tile only flushes
+    if (!bres && k >= nAk) {
+      resolve_b();
+      ntot = nAk + nBk;
     }
-    if (b != cur_b || seg != cur_seg) {
-      if (cur_b >= 0) flush(cur_b, cur_seg);
-      if (k == ntiles) break;
+    int ph = -1, b = -1, seg = -1, tis = 0;
+    if (k < ntot) {
+      where(wk, k);
+      ph = wk.ph;
+      b = wk.b;
+      seg = wk.seg;
+      tis = wk.tis;
+    }
+    if (ph != cur_ph || b != cur_b || seg != cur_seg) {
+      if (cur_b >= 0) flush(cur_ph, cur_b, cur_seg);
+      if (k >= ntot) break;
+      cur_ph = ph;
       cur_b = b;
       cur_seg = seg;
       // Q fragments (B operand of QK^T): Q[head n % G][k-chunk], this thread's column n = gq
@@ -665,7 +794,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       m0 = m1 = -INFINITY;
       l0 = l1 = 0.f;
     }
-    const int cnt = cnts[b];
+    const int4 in = info[b];
+    const int cnt = ph ? in.w : in.z;
     const int nvalid = min(kTile, cnt - tis * kTile);
     const int s = (int)(k % kStages);
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
@@ -680,10 +810,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       for (int x = 0; x < 4; ++x) sacc[mt][x] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
-        uint32_t a0, a1, a2, a3;
+        uint32_t a0r, a1r, a2r, a3r;
         const int row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        ldsm_x4(S::at(stK, row, ks * 2 + (lane >> 4)), a0, a1, a2, a3);
-        mma_bf16(sacc[mt], a0, a1, a2, a3, qf[ks][0], qf[ks][1]);
+        ldsm_x4(S::at(stK, row, ks * 2 + (lane >> 4)), a0r, a1r, a2r, a3r);
+        mma_bf16(sacc[mt], a0r, a1r, a2r, a3r, qf[ks][0], qf[ks][1]);
       }
     }
     // ---- online softmax over the tile's tokens, per column ----
@@ -765,17 +895,27 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
 
 template <int D, int G>
 size_t attn_smem_bytes(int B) {
-  return 1024 + (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + (size_t)kPtSmem * sizeof(int32_t) +
-         (size_t)(2 * B + 1) * sizeof(int32_t);
+  return 1024 + (size_t)AttnShape<D>::RING_BYTES + AttnShape<D>::BAR_BYTES + 16 + (size_t)B * sizeof(int4) +
+         (size_t)kPtSmem * sizeof(int32_t) + (size_t)(2 * B + 3) * sizeof(int32_t);
 }
 
-inline int attn_grid() {
-  static int spare = -1;
-  if (spare < 0) {
+// SMs left out of a5's persistent grid.  With the early-known rows (seq_len
+// given) one SM is left free by default: the producer of I_f ends with one
+// CTA per sequence building I_f, and an a5 CTA that had to wait for that SM
+// would start its equal share of the work late and finish last.
+inline int attn_spare_env() {
+  static int spare = -2;
+  if (spare == -2) {
     const char *e = getenv("ZOOMR_ATTN_SPARE_SMS");  // A/B experiments only
-    spare = e ? atoi(e) : 0;
+    spare = e ? atoi(e) : -1;
   }
-  return num_sms() - spare;
+  return spare;
+}
+inline int attn_grid(bool early = false) {
+  const int env = attn_spare_env();
+  const int spare = env >= 0 ? env : (early ? 1 : 0);
+  const int g = num_sms() - spare;
+  return g > 0 ? g : 1;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -803,9 +943,10 @@ inline int encode_pool_map(CUtensorMap *m, const void *base, int d, uint64_t row
   return r == CUDA_SUCCESS ? 0 : 1;
 }
 
-inline size_t attn_ws_part_floats(const zoomr_geom *g) {
+inline size_t attn_ws_part_floats(const zoomr_geom *g, int32_t batch) {
   const int G = g->num_q_heads / g->num_kv_heads;
-  return (size_t)attn_grid() * kPairs * 2 * ((2 * G + 3) / 4 * 4 + G * g->head_dim);
+  const size_t slots = 2 * ((size_t)attn_grid() * kPairs + (size_t)batch * g->num_layers * g->num_kv_heads);
+  return slots * ((2 * G + 3) / 4 * 4 + G * g->head_dim);
 }
 
 }  // namespace zoomr
@@ -814,7 +955,7 @@ using namespace zoomr;
 
 extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch) {
   if (check_geom(geom) || batch < 1) return 0;
-  const size_t part = attn_ws_part_floats(geom) * sizeof(float);
+  const size_t part = attn_ws_part_floats(geom, batch) * sizeof(float);
   const size_t cnt = (size_t)batch * geom->num_layers * geom->num_kv_heads * sizeof(int32_t);
   return ((part + 255) / 256) * 256 + cnt;
 }
@@ -822,6 +963,7 @@ extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t bat
 extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
                                         const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                         const int32_t *index_count, int32_t index_capacity,
+                                        const int32_t *seq_len, int32_t sink, int32_t window,
                                         float softmax_scale, float *out, void *workspace,
                                         size_t workspace_bytes, int32_t *dev_status, void *stream) {
   int rc = check_geom(geom);
@@ -830,6 +972,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
       index_capacity < 1 || !out || !workspace || kv->num_pages < 1 || kv->max_pages < 1)
     return ZOOMR_ERR_INVALID_ARG;
   if (batch > 65536) return ZOOMR_ERR_UNSUPPORTED;
+  if (seq_len && (sink < 0 || window < 0)) return ZOOMR_ERR_INVALID_ARG;
   const size_t need = zoomr_attn_workspace_bytes(geom, batch);
   if (workspace_bytes < need) return ZOOMR_ERR_WORKSPACE;
   AttnParams prm;
@@ -844,7 +987,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   prm.count = index_count;
   prm.cap = index_capacity;
   prm.out = out;
-  const size_t part = attn_ws_part_floats(geom) * sizeof(float);
+  const size_t part = attn_ws_part_floats(geom, batch) * sizeof(float);
   prm.ws_part = (float *)workspace;
   prm.ws_cnt = (int32_t *)((char *)workspace + ((part + 255) / 256) * 256);
   prm.B = batch;
@@ -856,10 +999,13 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   for (int sft = 0; sft < 31; ++sft)
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+  prm.seq_len = seq_len;
+  prm.sink = sink;
+  prm.window = window;
   prm.status = dev_status;
   const int G = geom->num_q_heads / geom->num_kv_heads;
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = attn_grid();
+  const int grid = attn_grid(seq_len != nullptr);
   TmaMaps maps;
   {
     const uint64_t rows = (uint64_t)geom->num_layers * kv->num_pages * geom->num_kv_heads * geom->page_size;

@@ -28,7 +28,8 @@ class ZoomrStep:
     """Device state + launch sequence of one (rank-local) decode step."""
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
-                 params: StepParams, device="cuda", debug_outputs: bool = False, use_phys: bool = False):
+                 params: StepParams, device="cuda", debug_outputs: bool = False, use_phys: bool = False,
+                 early_known: bool = True):
         self.shape, self.batch, self.params = shape, batch, params
         self.max_summaries, self.cap = max_summaries, index_capacity
         dev = torch.device(device)
@@ -52,6 +53,7 @@ class ZoomrStep:
             self.topk = torch.zeros(batch, L * Hq, params.top_k, dtype=torch.int32, device=dev)
         self.graph = None
         self.use_phys = use_phys  # fused select writes page-resolved rows for a5
+        self.early_known = early_known  # a5 attends I_p, I_w before waiting for I_f
 
     # -- a1: mean keys for a list of closed summaries (b, i) --------------------
     def update_mean_keys(self, kv, seg, items: torch.Tensor):
@@ -89,9 +91,7 @@ class ZoomrStep:
                            self.count, self.sel_workspace, partial=self.partial,
                            agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
                            dev_status=self.status, index_phys=self.index_phys if self.use_phys else None)
-            Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
-                                 self.out, self.workspace, dev_status=self.status,
-                                 index_phys=self.index_phys if self.use_phys else None)
+            self.attend(q, kv, seq_len)
             return self.out
         if close_items is not None and close_items.numel():
             self.update_mean_keys(kv, seg, close_items)
@@ -103,9 +103,19 @@ class ZoomrStep:
             Z.select_topc(self.partial, nsum, p.c, self.flags, self.agreeability, self.status)
         Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count,
                       self.status)
-        Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
-                             self.out, self.workspace, dev_status=self.status)
+        self.attend(q, kv, seq_len, phys=False)
         return self.out
+
+    def attend(self, q, kv, seq_len, phys=None):
+        """a5 over the current I_f.  With early_known, I_p and I_w (known from
+        T alone) are attended while the producer of I_f is still running."""
+        k_pool, v_pool, page_table = kv
+        use_phys = self.use_phys if phys is None else phys
+        p = self.params
+        Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
+                             self.out, self.workspace, dev_status=self.status,
+                             index_phys=self.index_phys if use_phys else None,
+                             seq_len=seq_len if self.early_known else None, sink=p.sink, window=p.window)
 
     def launches_per_step(self, update_selection=True, close=False, fused=True) -> int:
         """Kernel launches one run() enqueues (a2 = zero + score when not fused)."""

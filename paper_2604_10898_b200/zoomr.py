@@ -47,6 +47,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
+ABI_VERSION = 2  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -65,7 +66,7 @@ def lib():
         L.zoomr_build_index.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]
         L.zoomr_attn_workspace_bytes.argtypes = [vp, i32]
         L.zoomr_attn_workspace_bytes.restype = sz
-        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, vp, vp, sz,
+        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, vp, vp, sz,
                                                vp, vp]
         L.zoomr_select_workspace_bytes.argtypes = [vp, i32, i32]
         L.zoomr_select_workspace_bytes.restype = sz
@@ -78,6 +79,9 @@ def lib():
         for fn in (L.zoomr_update_mean_keys, L.zoomr_score, L.zoomr_select_topc,
                    L.zoomr_build_index, L.zoomr_sparse_decode_attn):
             fn.restype = C.c_int
+        if L.zoomr_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.zoomr_abi_version()}, this binding expects {ABI_VERSION}: "
+                              "rebuild with __graft_entry__.build()")
         _lib = L
     return _lib
 
@@ -190,14 +194,19 @@ def attn_workspace_bytes(shape: Shape, batch: int) -> int:
 
 
 def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out,
-                       workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None):
-    """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once."""
+                       workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
+                       seq_len=None, sink=0, window=0):
+    """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once.
+
+    seq_len/sink/window (optional): `index` is a4's output for these values, so
+    I_p and I_w are attended before the kernel waits for I_f (see zoomr.h)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
     rc = lib().zoomr_sparse_decode_attn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
                                         C.byref(kv), _ptr(index, torch.int32, "index"),
                                         _ptr(index_phys, torch.int32, "index_phys"),
                                         _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                        _ptr(seq_len, torch.int32, "seq_len"), int(sink), int(window),
                                         C.c_float(sc), _ptr(out, torch.float32, "out"),
                                         _ptr(workspace, None, "workspace"), workspace.numel() *
                                         workspace.element_size(),

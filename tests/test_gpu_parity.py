@@ -143,3 +143,30 @@ def test_degenerate_cases(fused):
         st = PY.make_step(inp)
         PY.run_full(inp, st, fused=fused)
         PY.check_sequence(inp, st, 0, {})
+
+
+@pytest.mark.parametrize("variant", ["tiny_b5_jitter", "tiny_window_ge_T", "tiny_c0", "tiny_b320", "8b16k"])
+def test_early_known_rows_equal_index_only(variant):
+    """a5 with seq_len/sink/window (I_p and I_w attended before the wait, merged
+    with the rest of I_f afterwards) vs a5 reading every row from the index:
+    the same softmax over the same rows, only the merge order differs."""
+    import dataclasses
+    base = S.CONFIGS["tiny"]
+    cfg = {"tiny_b5_jitter": dataclasses.replace(base, batch=5, jitter=True),
+           "tiny_window_ge_T": dataclasses.replace(base, batch=2, window=300, sink=7),
+           "tiny_c0": dataclasses.replace(base, c=0, sink=0),
+           # more segments (640) than math warps: one warp's range spans >= 3 segments per phase
+           "tiny_b320": dataclasses.replace(base, batch=320, window=96),
+           "8b16k": S.CONFIGS["8b16k"]}[variant]
+    inp = S.generate(cfg, device="cuda", seed=31)
+    cap = 8192 if variant == "8b16k" else None
+    a, b = PY.make_step(inp, capacity=cap), PY.make_step(inp, capacity=cap)
+    b.early_known = False
+    PY.run_full(inp, a, fused=True)
+    PY.run_full(inp, b, fused=True)
+    assert torch.equal(a.index, b.index) and torch.equal(a.count, b.count)
+    assert (a.out - b.out).abs().max().item() <= 1e-5
+    rep = {}
+    B = inp.q.shape[0]
+    for s in sorted({min(x, B - 1) for x in (0, 1, 2, B // 2, B - 1)}):
+        PY.check_sequence(inp, a, s, rep)

@@ -6,7 +6,7 @@ from paper_2604_10898_b200 import zoomr as Z
 from paper_2604_10898_b200.step import StepParams, ZoomrStep
 
 def run(variant, R=4, K=200):
-    cfg = S.CONFIGS[os.environ.get("WL", "8b16k")]
+    cfg = S.config_by_name(os.environ.get("WL", "8b16k"))
     shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
     gs = []
     for r in range(R):
@@ -24,7 +24,8 @@ def run(variant, R=4, K=200):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / K
 
-VARIANTS = {"phys": dict(use_phys=True), "nophys": dict(use_phys=False)}
+VARIANTS = {"phys": dict(use_phys=True), "nophys": dict(use_phys=False),
+            "early": dict(early_known=True), "late": dict(early_known=False)}
 for name in os.environ.get("VARS", "nophys,phys").split(","):
     v = VARIANTS[name]
     print(name, round(run(v), 2), "us/step", flush=True)

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import zoomr_synth as S
 from paper_2604_10898_b200 import zoomr as Z
 from paper_2604_10898_b200.step import StepParams, ZoomrStep
-cfg = S.CONFIGS[os.environ.get("WL", "8b16k")]
+cfg = S.config_by_name(os.environ.get("WL", "8b16k"))
 inp = S.generate(cfg, device="cuda")
 shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
 st = ZoomrStep(shape, 1, inp.bounds.shape[1], cfg.T, StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window))

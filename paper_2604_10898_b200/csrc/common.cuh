@@ -99,3 +99,73 @@ inline int check_geom(const zoomr_geom *g) {
 }
 
 }  // namespace zoomr
+
+// ---- experiment builds only (-DZOOMR_TIMELINE, tools/timeline.py) ----------
+// TL(i): lane 0 records %globaltimer into the min / max of slot i of the
+// translation unit's g_tl (declare with ZOOMR_TL_STORAGE(name), which also
+// exports zoomr_tl_<name>(out, reset)).  Compiled out of the product library.
+#ifdef ZOOMR_TIMELINE
+#define ZOOMR_TL_STORAGE(name)                                                                    \
+  namespace zoomr {                                                                               \
+  static __device__ unsigned long long g_tl[2 * 16];                                              \
+  static __device__ unsigned long long g_tl_cta[1024][4]; /* per CTA: smid, start, end, - */       \
+  static __device__ unsigned long long g_tl_warp[4096][8]; /* per math warp: free-form counters */  \
+  }                                                                                               \
+  extern "C" int zoomr_tl_warp_##name(unsigned long long *out) {                                  \
+    return cudaMemcpyFromSymbol(out, zoomr::g_tl_warp, sizeof(zoomr::g_tl_warp)) == cudaSuccess ? 0 : 8; \
+  }                                                                                               \
+  extern "C" int zoomr_tl_cta_##name(unsigned long long *out) {                                   \
+    return cudaMemcpyFromSymbol(out, zoomr::g_tl_cta, sizeof(zoomr::g_tl_cta)) == cudaSuccess ? 0 : 8; \
+  }                                                                                               \
+  extern "C" int zoomr_tl_##name(unsigned long long *out, int reset) {                            \
+    if (cudaMemcpyFromSymbol(out, zoomr::g_tl, sizeof(zoomr::g_tl)) != cudaSuccess) return 8;    \
+    if (reset) {                                                                                  \
+      unsigned long long h[2 * 16];                                                               \
+      for (int i = 0; i < 16; ++i) { h[2 * i] = ~0ull; h[2 * i + 1] = 0; }                        \
+      if (cudaMemcpyToSymbol(zoomr::g_tl, h, sizeof(h)) != cudaSuccess) return 8;                \
+      void *pc = nullptr;                                                                         \
+      if (cudaGetSymbolAddress(&pc, zoomr::g_tl_cta) != cudaSuccess) return 8;                    \
+      if (cudaMemset(pc, 0, sizeof(zoomr::g_tl_cta)) != cudaSuccess) return 8;                    \
+      if (cudaGetSymbolAddress(&pc, zoomr::g_tl_warp) != cudaSuccess) return 8;                   \
+      if (cudaMemset(pc, 0, sizeof(zoomr::g_tl_warp)) != cudaSuccess) return 8;                   \
+    }                                                                                             \
+    return 0;                                                                                     \
+  }
+#define TL(i)                                                                  \
+  do {                                                                         \
+    if ((threadIdx.x & 31) == 0) {                                             \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      atomicMin(&g_tl[2 * (i)], t_);                                           \
+      atomicMax(&g_tl[2 * (i) + 1], t_);                                       \
+    }                                                                          \
+  } while (0)
+// TL_CTA(k): per-CTA record (k = 1 start, 2 end: max over the CTA's warps), slot 0 = %smid
+#define TL_CTA(k)                                                                          \
+  do {                                                                                     \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) {                                    \
+      unsigned long long t_;                                                               \
+      unsigned sm_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                                     \
+      g_tl_cta[blockIdx.x][0] = sm_;                                                       \
+      if ((k) == 1) g_tl_cta[blockIdx.x][1] = t_;                                          \
+      else atomicMax(&g_tl_cta[blockIdx.x][k], t_);                                        \
+    }                                                                                      \
+  } while (0)
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t_;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+  return t_;
+}
+#define TLW_ADD(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096) atomicAdd(&g_tl_warp[w][f], (unsigned long long)(v)); } while (0)
+#define TLW_SET(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096) g_tl_warp[w][f] = (unsigned long long)(v); } while (0)
+#define TL_NOW() tl_now()
+#else
+#define ZOOMR_TL_STORAGE(name)
+#define TL(i) do { } while (0)
+#define TL_CTA(k) do { } while (0)
+#define TLW_ADD(w, f, v) do { } while (0)
+#define TLW_SET(w, f, v) do { } while (0)
+#define TL_NOW() 0ull
+#endif

@@ -26,6 +26,8 @@
 // all-reduce between a2 and a3 and uses the standalone entry points.
 #include "select_common.cuh"
 
+ZOOMR_TL_STORAGE(fused)
+
 namespace zoomr {
 
 
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
   allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
+  TL(0);
   const int lg = blockIdx.x, b = blockIdx.y;
   const int l = lg / p.Hkv, g = lg - l * p.Hkv;
   const int Hq = p.Hkv * G, V = p.L * Hq, MS = p.max_summaries;
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   // bar.sync orders the CTA's writes before thread 0's acq_rel ticket (release,
   // cumulative at gpu scope); the winner's acquire + bar.sync order its reads after.
   __syncthreads();
+  if (threadIdx.x == 0) TL(1);
   if (threadIdx.x == 0) {
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ws_ticket + b) : "memory");
@@ -130,6 +134,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   }
   __syncthreads();
   if (!ticket_last) return;
+  if (threadIdx.x == 0) TL(2);
   if (p.stop_after == 1) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
 
   // ---- aggregation (a2, cross-head / cross-layer), exact integer atomics --------
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     }
   }
   if (p.stop_after == 2) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
+  if (threadIdx.x == 0) TL(3);
   // ---- a3: consensus top-c ----------------------------------------------------------
   block_topc(v, A, nt, p.c, fl, hist, grp, scratch, p.agreeability ? p.agreeability + b : nullptr);
 
@@ -169,6 +175,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   for (int i = threadIdx.x; i < MS; i += blockDim.x) fo[i] = i < nt ? fl[i] : 0;
   __syncthreads();
   if (p.stop_after == 3) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
+  if (threadIdx.x == 0) TL(4);
   // ---- a4: the index set --------------------------------------------------------------
   if (T < 1) {
     if (threadIdx.x == 0) {
@@ -182,6 +189,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   }
   if (threadIdx.x == 0) p.ws_ticket[b] = 0;  // ready for the next step
   __syncthreads();
+  if (threadIdx.x == 0) TL(5);
 }
 
 template <int D, int G>

@@ -47,11 +47,6 @@ constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addr
 constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
 constexpr int kStages = 3;  // ring depth per pair
 constexpr int kPtSmem = 4096; // page-table entries staged in shared memory when they fit
-constexpr int kBoxes = 5;     // TMA box heights 16, 8, 4, 2, 1 rows
-#ifndef ZOOMR_MIN_BOX
-#define ZOOMR_MIN_BOX 8       // smallest TMA box (8: the < 8-row leftovers go by cp.async; 1: all TMA, measured slower)
-#endif
-constexpr int kMinBox = ZOOMR_MIN_BOX;
 
 template <int D>
 struct AttnShape {
@@ -77,8 +72,7 @@ struct AttnShape {
 };
 
 struct TmaMaps {
-  // 2D [total rows][D] views of the pools; box heights 16 >> i rows (16, 8, 4, 2, 1)
-  CUtensorMap k[kBoxes], v[kBoxes];
+  CUtensorMap k16, k8, v16, v8;  // 2D [total rows][D] views of the pools, boxes of 16 / 8 rows
 };
 
 struct AttnParams {
@@ -463,9 +457,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         }
         if (cok) grow = (((int64_t)ac.l * p.num_pages + page) * p.Hkv + ac.g) * p.P + ac.slot;
       }
-      // runs of consecutive tokens in one page -> TMA boxes of 16 rows, then the
-      // remainder as at most one box each of 8, 4, 2 and 1 rows (binary
-      // decomposition, kMinBox bounds it); rows past the end: cp.async zero-fill
+      // runs of consecutive tokens in one page -> boxes of 16 / 8 rows; the rest by cp.async.
+      // (A table of 16/8/4/2/1-row boxes without cp.async measured 1-2 us slower per launch.)
       const int ptok = __shfl_up_sync(0xffffffffu, ac.tok, 1);
       const int ppage = __shfl_up_sync(0xffffffffu, page, 1);
       const int pok = __shfl_up_sync(0xffffffffu, cok, 1);
@@ -477,31 +470,23 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       const unsigned after = (startm | ~validm) & ~upto;
       const int re = after ? __ffs(after) - 1 : 32;                // one past my run's last slot
       const int pos = lane - rs, len = re - rs;
-      const int n16 = len & ~15, rem = (len & 15) & ~(kMinBox - 1), q = pos - n16;
-      // my box: height h (0 = none); TMA needs 128-byte aligned destinations: d >= 64 only
-      int h = 0;
-      if (S::SWZ && cok) {
-        if (pos < n16) h = (pos & 15) == 0 ? 16 : 0;
-        else if ((rem & 8) && q == 0) h = 8;
-        else if ((rem & 4) && q == (rem & 8)) h = 4;
-        else if ((rem & 2) && q == (rem & 12)) h = 2;
-        else if ((rem & 1) && q == (rem & 14)) h = 1;
-      }
-      const bool byhand = !cok || !S::SWZ || pos >= n16 + rem;
-      int hsum = h;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-      const uint32_t tx = (uint32_t)(hsum * S::RB * 2);
+      const int n16 = (len >> 4) << 4, n8 = ((len & 15) >> 3) << 3;
+      // TMA boxes need 128-byte aligned destinations: d >= 64 only (d < 64 configs are toy-sized)
+      const bool lead16 = S::SWZ && cok && pos < n16 && (pos & 15) == 0;
+      const bool lead8 = S::SWZ && cok && n8 && pos == n16;
+      const bool byhand = !cok || !S::SWZ || pos >= n16 + n8;
+      const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8);
+      const uint32_t tx = (uint32_t)((__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
       const int s = (int)(k % kStages);
       mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1));
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
       const uint32_t stV = stK + S::TILE_BYTES;
+      if (k == 0) TL(7);
       if (lane == 0) mbar_arrive_expect_tx(&fullp[s], tx);
       __syncwarp();
-      if (h) {
-        const int bi = 4 - (31 - __clz(h));  // 16 -> 0, 8 -> 1, 4 -> 2, 2 -> 3, 1 -> 4
-        const CUtensorMap *mk = &maps.k[bi];
-        const CUtensorMap *mv = &maps.v[bi];
+      if (lead16 || lead8) {
+        const CUtensorMap *mk = lead16 ? &maps.k16 : &maps.k8;
+        const CUtensorMap *mv = lead16 ? &maps.v16 : &maps.v8;
 #pragma unroll
         for (int rg = 0; rg < S::NREG; ++rg) {
           // destination = the row's unswizzled start; the TMA unit applies the 128-byte swizzle
@@ -541,9 +526,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       }
 #ifdef ZOOMR_TIMELINE
       const unsigned tl_cp = __ballot_sync(0xffffffffu, byhand && cok);
-      const unsigned tl_bx = __ballot_sync(0xffffffffu, h != 0);
       TLW_ADD(gw, 4, __popc(tl_cp));
-      TLW_ADD(gw, 5, __popc(tl_bx));
+      TLW_ADD(gw, 5, __popc(m16) + __popc(m8));
 #endif
       q0 = q1;
       q1 = q2;
@@ -1058,9 +1042,9 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     const uint64_t rows = (uint64_t)geom->num_layers * kv->num_pages * geom->num_kv_heads * geom->page_size;
     if (rows >= (1ull << 31)) return ZOOMR_ERR_UNSUPPORTED;  // TMA row coordinate is int32
     const int d = geom->head_dim;
-    for (int i = 0; i < kBoxes && (16 >> i) >= kMinBox; ++i)  // only the box heights in use
-      if (encode_pool_map(&maps.k[i], kv->k, d, rows, 16 >> i) || encode_pool_map(&maps.v[i], kv->v, d, rows, 16 >> i))
-        return ZOOMR_ERR_CUDA;
+    if (encode_pool_map(&maps.k16, kv->k, d, rows, 16) || encode_pool_map(&maps.k8, kv->k, d, rows, 8) ||
+        encode_pool_map(&maps.v16, kv->v, d, rows, 16) || encode_pool_map(&maps.v8, kv->v, d, rows, 8))
+      return ZOOMR_ERR_CUDA;
   }
 #define ZOOMR_AT(DD, GG)                                                                 \
   do {                                                                                   \

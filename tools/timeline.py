@@ -25,7 +25,8 @@ def read(fn, reset):
 
 
 NAMES = {"select": ["start", "front_end", "tail_start", "collected", "topc_done", "end"],
-         "a5": ["start", "prologue", "B_known", "first_tile", "first_B_tile", "math_done", "prod_done"]}
+         "a5": ["start", "prologue", "B_known", "first_tile", "first_B_tile", "math_done", "prod_done",
+                "first_issue"]}
 for var in os.environ.get("VARS", "early,late").split(","):
     sets = []
     for r in range(4):
@@ -106,7 +107,9 @@ if os.environ.get("WARPS"):
             if r[0]:
                 recs.append(dict(rep=i, w=w, end=(r[0] - f[0]) / 1e3, tiles=r[1], merges=r[2], merge_us=r[3] / 1e3,
                                  cp_rows=r[4], boxes=r[5], pend=(r[6] - f[0]) / 1e3 if r[6] else 0, flushes=r[7]))
-    import numpy as np
+    import json, numpy as np
+    os.makedirs("gpurun_out", exist_ok=True)
+    json.dump(recs, open("gpurun_out/timeline_warps.json", "w"))
     keys = ["end", "tiles", "merges", "merge_us", "cp_rows", "boxes", "pend", "flushes"]
     M = np.array([[r[k] for k in keys] for r in recs], dtype=np.float64)
     print("per-warp stats over", len(recs), "warp-steps")

@@ -108,6 +108,16 @@ inline int check_geom(const zoomr_geom *g) {
 #define ZOOMR_TL_STORAGE(name)                                                                    \
   namespace zoomr {                                                                               \
   static __device__ unsigned long long g_tl[2 * 16];                                              \
+  static __device__ int g_tl_on; /* marks are recorded only while armed */                        \
+  }                                                                                               \
+  extern "C" int zoomr_tl_arm_##name(int on, void *stream) {                                      \
+    static int v[2] = {0, 1};                                                                     \
+    return cudaMemcpyToSymbolAsync(zoomr::g_tl_on, &v[on ? 1 : 0], sizeof(int), 0,                \
+                                   cudaMemcpyHostToDevice, (cudaStream_t)stream) == cudaSuccess ? 0 : 8; \
+  }                                                                                               \
+  ZOOMR_TL_STORAGE_REST(name)
+#define ZOOMR_TL_STORAGE_REST(name)                                                               \
+  namespace zoomr {                                                                               \
   static __device__ unsigned long long g_tl_cta[1024][4]; /* per CTA: smid, start, end, - */       \
   static __device__ unsigned long long g_tl_warp[4096][8]; /* per math warp: free-form counters */  \
   }                                                                                               \
@@ -133,7 +143,7 @@ inline int check_geom(const zoomr_geom *g) {
   }
 #define TL(i)                                                                  \
   do {                                                                         \
-    if ((threadIdx.x & 31) == 0) {                                             \
+    if ((threadIdx.x & 31) == 0 && tl_on_) {                \
       unsigned long long t_;                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
       atomicMin(&g_tl[2 * (i)], t_);                                           \
@@ -143,7 +153,7 @@ inline int check_geom(const zoomr_geom *g) {
 // TL_CTA(k): per-CTA record (k = 1 start, 2 end: max over the CTA's warps), slot 0 = %smid
 #define TL_CTA(k)                                                                          \
   do {                                                                                     \
-    if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) {                                    \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024 && tl_on_) {       \
       unsigned long long t_;                                                               \
       unsigned sm_;                                                                        \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
@@ -153,13 +163,14 @@ inline int check_geom(const zoomr_geom *g) {
       else atomicMax(&g_tl_cta[blockIdx.x][k], t_);                                        \
     }                                                                                      \
   } while (0)
+#define TL_INIT() const bool tl_on_ = *(volatile int *)&g_tl_on  // once per kernel: marks only while armed
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t_;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
   return t_;
 }
-#define TLW_ADD(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096) atomicAdd(&g_tl_warp[w][f], (unsigned long long)(v)); } while (0)
-#define TLW_SET(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096) g_tl_warp[w][f] = (unsigned long long)(v); } while (0)
+#define TLW_ADD(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096 && tl_on_) atomicAdd(&g_tl_warp[w][f], (unsigned long long)(v)); } while (0)
+#define TLW_SET(w, f, v) do { if ((threadIdx.x & 31) == 0 && (w) < 4096 && tl_on_) g_tl_warp[w][f] = (unsigned long long)(v); } while (0)
 #define TL_NOW() tl_now()
 #else
 #define ZOOMR_TL_STORAGE(name)
@@ -168,4 +179,5 @@ __device__ __forceinline__ unsigned long long tl_now() {
 #define TLW_ADD(w, f, v) do { } while (0)
 #define TLW_SET(w, f, v) do { } while (0)
 #define TL_NOW() 0ull
+#define TL_INIT() do { } while (0)
 #endif

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
   const int LH = p.L * p.Hkv;
+  TL_INIT();
   if (threadIdx.x == 0) {
     TL(0);
     TL_CTA(1);

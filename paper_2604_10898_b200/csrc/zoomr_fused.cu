@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
   allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
+  TL_INIT();
   TL(0);
   const int lg = blockIdx.x, b = blockIdx.y;
   const int l = lg / p.Hkv, g = lg - l * p.Hkv;

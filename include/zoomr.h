@@ -175,7 +175,9 @@ size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
  * from T alone -- before it waits for the producer of I_f (it is launched with
  * programmatic dependent launch), so that part of the gather overlaps the
  * selection; the rest of I_f is read from `index` afterwards.  Only this
- * kernel's workspace is written before the wait.  NULL: every row comes from
+ * kernel's workspace is written before the wait, so the kernel preceding it on
+ * the stream must not be another zoomr_sparse_decode_attn call that uses the
+ * same workspace (normally it is zoomr_select_fused or zoomr_build_index).  NULL: every row comes from
  * `index` (any sorted or unsorted list of positions is then accepted). */
 int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
                              const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,

@@ -119,14 +119,46 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef ZOOMR_WATCHDOG
+// experiment builds only: a spin lasting > 0.5 s writes (site, a, b) for its
+// (block, warp) into host-mapped memory (zoomr_watchdog_set), readable while hung
+__device__ unsigned long long *g_wd_host;  // [1024 blocks][8 warps][4]
+__device__ __noinline__ void wd_fire(int site, int a, int b) {
+  if (g_wd_host && blockIdx.x < 1024) {
+    volatile unsigned long long *r = g_wd_host + ((size_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 4;
+    r[0] = (unsigned)site;
+    r[1] = (unsigned)a;
+    r[2] = (unsigned)b;
+    r[3] = 1;
+    __threadfence_system();
+  }
+}
+__device__ __forceinline__ unsigned long long wd_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define WD_DECL unsigned long long wd_t0_ = 0
+#define WD_TICK(site, a, b)                                                                  \
+  do {                                                                                       \
+    const unsigned long long wd_t_ = wd_now();                                               \
+    if (!wd_t0_) wd_t0_ = wd_t_;                                                             \
+    else if (wd_t_ - wd_t0_ > 500000000ull) { wd_fire(site, (int)(a), (int)(b)); wd_t0_ = wd_t_; } \
+  } while (0)
+#else
+#define WD_DECL do { } while (0)
+#define WD_TICK(site, a, b) do { } while (0)
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int site = 0) {
   uint32_t done;
+  WD_DECL;
   do {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    if (!done) WD_TICK(site, parity, 0);
   } while (!done);
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
@@ -331,7 +363,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bready);  // release: the schedule above is visible to the waiters
     } else {
-      mbar_wait(bready, 0);  // acquire (suspends instead of hammering shared memory)
+      mbar_wait(bready, 0, 7);  // acquire (suspends instead of hammering shared memory)
     }
     __syncwarp();
     sB.T_tot = prefB[p.B];
@@ -479,7 +511,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8);
       const uint32_t tx = (uint32_t)((__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
       const int s = (int)(k % kStages);
-      mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1));
+      mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1), 6000000 + (int)k);
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
       const uint32_t stV = stK + S::TILE_BYTES;
       if (k == 0) TL(7);
@@ -828,7 +860,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     const int cnt = ph ? in.w : in.z;
     const int nvalid = min(kTile, cnt - tis * kTile);
     const int s = (int)(k % kStages);
-    mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1));
+    mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1), 5000000 + (int)k);
     if (k == 0) TL(3);
     if (k == nAk) TL(4);
     const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
@@ -1091,3 +1123,9 @@ extern "C" const char *zoomr_status_str(int status) {
 }
 
 extern "C" int zoomr_abi_version(void) { return ZOOMR_ABI_VERSION; }
+
+#ifdef ZOOMR_WATCHDOG
+extern "C" int zoomr_watchdog_set(void *host_mapped_dev_ptr) {
+  return cudaMemcpyToSymbol(zoomr::g_wd_host, &host_mapped_dev_ptr, sizeof(void *)) == cudaSuccess ? 0 : 8;
+}
+#endif

@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   int32_t *prefA = pts + (p.pt_smem ? kPtSmem : 0);        // [B+1] first phase-A tile of sequence b
   int32_t *prefB = prefA + p.B + 1;                        // [B+1] first phase-B tile
   int32_t *bstate = prefB + p.B + 1;                       // phase-B schedule: 0 unclaimed, 1 claimed
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: ptxas then treats it (and the pair's ring and
+  // barriers) as warp-uniform, which keeps the TMA issue's operands in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
   const int LH = p.L * p.Hkv;
   TL_INIT();
@@ -517,15 +519,23 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       if (k == 0) TL(7);
       if (lane == 0) mbar_arrive_expect_tx(&fullp[s], tx);
       __syncwarp();
-      if (lead16 || lead8) {
-        const CUtensorMap *mk = lead16 ? &maps.k16 : &maps.k8;
-        const CUtensorMap *mv = lead16 ? &maps.v16 : &maps.v8;
+      // one issue block per box height: the tensor map (like the barrier and the
+      // stage) is warp-uniform, so only the row and the destination vary per lane
+      if (lead16) {
 #pragma unroll
         for (int rg = 0; rg < S::NREG; ++rg) {
           // destination = the row's unswizzled start; the TMA unit applies the 128-byte swizzle
           const uint32_t off = (uint32_t)(rg * S::REG_BYTES + lane * S::RBR);
-          tma_load_2d(stK + off, mk, rg * S::BX, grow, &fullp[s]);
-          tma_load_2d(stV + off, mv, rg * S::BX, grow, &fullp[s]);
+          tma_load_2d(stK + off, &maps.k16, rg * S::BX, grow, &fullp[s]);
+          tma_load_2d(stV + off, &maps.v16, rg * S::BX, grow, &fullp[s]);
+        }
+      }
+      if (lead8) {
+#pragma unroll
+        for (int rg = 0; rg < S::NREG; ++rg) {
+          const uint32_t off = (uint32_t)(rg * S::REG_BYTES + lane * S::RBR);
+          tma_load_2d(stK + off, &maps.k8, rg * S::BX, grow, &fullp[s]);
+          tma_load_2d(stV + off, &maps.v8, rg * S::BX, grow, &fullp[s]);
         }
       }
       // leftover rows (and zero rows past the end): 16-byte cp.async, swizzle by hand

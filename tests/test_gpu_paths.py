@@ -1,0 +1,111 @@
+"""GPU parity of the less common paths through the C-ABI: other head dims and
+group sizes, the page-resolved rows (index_phys), a5 launched alone and
+back to back inside a CUDA graph, and the device status codes.
+
+Marked `gpu`: run on a B200 with the built libzoomr.so."""
+import dataclasses
+
+import pytest
+import torch
+
+import oracle
+import zoomr_synth as S
+from tests import parity as PY
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    oracle.build()
+    from paper_2604_10898_b200 import _build
+    _build.build()
+
+
+def _small(name, **kw):
+    base = dict(name=name, L=2, Hq=8, Hkv=2, d=64, T=2048, n_pairs=24, LR=60, LS=12, sink=4, window=96,
+                c=3, top_k=2, page=32, seed=41)
+    base.update(kw)
+    return S.Config(**base)
+
+
+@pytest.mark.parametrize("cfg", [
+    _small("d64_g4"),                                  # d = 64: one swizzled 64-column region, TMA boxes
+    _small("d128_g1", d=128, Hq=2, Hkv=2),             # G = 1
+    _small("d128_g8", d=128, Hq=16, Hkv=2),            # G = 8 (hi and lo in separate MMA n-tiles)
+    _small("d32_g2", d=32, Hq=4, Hkv=2, batch=3),      # d = 32: rows by cp.async only
+], ids=lambda c: c.name)
+@pytest.mark.parametrize("fused", [False, True])
+def test_head_dims_and_groups(cfg, fused):
+    inp = S.generate(cfg, device="cuda")
+    st = PY.make_step(inp)
+    PY.run_full(inp, st, fused=fused)
+    rep = {}
+    for b in range(inp.q.shape[0]):
+        PY.check_sequence(inp, st, b, rep)
+
+
+@pytest.mark.parametrize("cfg_name", ["tiny", "8b16k"])
+def test_page_resolved_rows_equal(cfg_name):
+    """The fused select's index_phys (page-resolved rows) drives a5 to the same
+    output as the page-table lookups, with and without the early rows."""
+    cfg = dataclasses.replace(S.CONFIGS[cfg_name], batch=2 if cfg_name == "tiny" else 1)
+    inp = S.generate(cfg, device="cuda", seed=8)
+    cap = 8192 if cfg_name == "8b16k" else None
+    a, b = PY.make_step(inp, capacity=cap), PY.make_step(inp, capacity=cap)
+    b.use_phys = True
+    for early in (True, False):
+        a.early_known = b.early_known = early
+        PY.run_full(inp, a, fused=True)
+        PY.run_full(inp, b, fused=True)
+        assert torch.equal(a.index, b.index) and torch.equal(a.count, b.count)
+        assert torch.equal(a.out, b.out), early
+    rep = {}
+    PY.check_sequence(inp, b, 0, rep)
+
+
+def test_attention_alone_back_to_back_in_a_graph():
+    """a5 launched repeatedly in one CUDA graph (programmatic launch edges between
+    consecutive a5 nodes): the self-resetting workspace keeps every launch exact."""
+    inp = S.generate(S.CONFIGS["8b16k"], device="cuda", seed=3)
+    st = PY.make_step(inp, capacity=8192)
+    PY.run_full(inp, st, fused=True)
+    ref = st.out.clone()
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    for early in (False, True):
+        st.early_known = early
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(8):
+                st.attend(inp.q, kv, inp.seq_len)
+        for _ in range(3):
+            st.out.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        st.check_status()
+        assert (st.out - ref).abs().max().item() <= 1e-5, early
+
+
+def test_device_status_codes():
+    """Data-dependent errors are recorded in the device status word (first wins):
+    I_f longer than the index capacity -> CAPACITY (list truncated to the capacity)."""
+    from paper_2604_10898_b200 import zoomr as Z
+    inp = S.generate(S.CONFIGS["tiny"], device="cuda", seed=2)
+    st = PY.make_step(inp, capacity=40)  # |I_f| of tiny is 82-106
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    st.run(inp.q, kv, seg, fused=True)
+    torch.cuda.synchronize()
+    assert int(st.status.item()) == Z.ERR_CAPACITY
+    assert int(st.count[0]) == 40
+    # an empty summary segment (s1 <= s0) -> EMPTY_SEGMENT
+    st2 = PY.make_step(inp)
+    bad = inp.bounds.clone()
+    bad[0, 3, 3] = bad[0, 3, 2]
+    st2.update_mean_keys(kv, (bad, inp.num_summaries, inp.seq_len), torch.tensor([[0, 3]], dtype=torch.int32,
+                                                                                 device="cuda"))
+    torch.cuda.synchronize()
+    assert int(st2.status.item()) == Z.ERR_EMPTY_SEGMENT

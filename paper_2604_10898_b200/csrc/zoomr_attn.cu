@@ -658,9 +658,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     const int nh = (G == 1) ? 1 : 2;  // heads held by an owner thread: n0 (and n0+1)
     int64_t wf0, wf1;
     int n0w, n1w;
+    bool final_out = false;
     if (bres) {
       seg_parts(b, seg, wf0, n0w, wf1, n1w);
-      if (n0w + n1w == 1) {  // this warp is the segment's only part: final output
+      final_out = n0w + n1w == 1;
+      if (final_out) {  // this warp is the segment's only part: final output
         const int l = seg / p.Hkv, g = seg - l * p.Hkv;
         float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
         if (owner) {
@@ -676,10 +678,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
             }
           }
         }
-        return;
+        if (npend == 0) return;  // else: still count the pending phase-A partials below
       }
     }
-    {  // partial
+    if (!final_out) {  // partial
       float *ps = p.ws_part + part_slot(ph, gw, b, seg) * SLOT;
       if (owner) {
         if (gq == 0) {
@@ -710,11 +712,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     // count the pending phase-A partials (segments of the A range in order), then
     // this one; the last arriving part of a segment merges all of its parts
     int64_t t = a0;
-    const int narr = npend + 1;
+    const int npa = npend, narr = npend + (final_out ? 0 : 1);  // pending phase-A partials first, then this one
     npend = 0;
     for (int it = 0; it < narr; ++it) {
       int xb = b, xs = seg;
-      if (it + 1 < narr) {
+      if (it < npa) {
         int xt, xn;
         sA.locate(t, xb, xs, xt, xn);
         t += xn - xt;  // first tile of the next segment

@@ -145,7 +145,8 @@ def test_degenerate_cases(fused):
         PY.check_sequence(inp, st, 0, {})
 
 
-@pytest.mark.parametrize("variant", ["tiny_b5_jitter", "tiny_window_ge_T", "tiny_c0", "tiny_b320", "8b16k"])
+@pytest.mark.parametrize("variant", ["tiny_b5_jitter", "tiny_window_ge_T", "tiny_c0", "tiny_b320", "tiny_b320_nosum",
+                                     "8b16k"])
 def test_early_known_rows_equal_index_only(variant):
     """a5 with seq_len/sink/window (I_p and I_w attended before the wait, merged
     with the rest of I_f afterwards) vs a5 reading every row from the index:
@@ -157,6 +158,9 @@ def test_early_known_rows_equal_index_only(variant):
            "tiny_c0": dataclasses.replace(base, c=0, sink=0),
            # more segments (640) than math warps: one warp's range spans >= 3 segments per phase
            "tiny_b320": dataclasses.replace(base, batch=320, window=96),
+           # no summaries and sink + window = one tile: I_f is phase A only (no phase-B
+           # parts), with warps holding two phase-A segments
+           "tiny_b320_nosum": dataclasses.replace(base, batch=320, n_pairs=0, sink=4, window=28),
            "8b16k": S.CONFIGS["8b16k"]}[variant]
     inp = S.generate(cfg, device="cuda", seed=31)
     cap = 8192 if variant == "8b16k" else None

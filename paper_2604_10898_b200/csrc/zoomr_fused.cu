@@ -60,6 +60,7 @@ struct FusedParams {
   int32_t L, Hkv, P;
   int32_t *status;
   int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
+  int32_t designated_tail;  // the grid is resident at once: the last-launched CTA of b runs a3/a4
 };
 
 template <int D, int G>
@@ -128,6 +129,26 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   // cumulative at gpu scope); the winner's acquire + bar.sync order its reads after.
   __syncthreads();
   if (threadIdx.x == 0) TL(1);
+  if (p.designated_tail) {
+  // The CTA launched last for sequence b carries on: the others count
+  // themselves with a fire-and-forget release add and exit at once (their SMs
+  // go to a5 a round trip earlier); it waits (acquire) until all have counted.
+  // Used only when the whole grid is resident at once (host check), so the
+  // CTAs it waits for are running.
+  const int nlg = p.L * p.Hkv;
+  if (lg != nlg - 1) {
+    if (threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ws_ticket + b) : "memory");
+    return;
+  }
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ws_ticket + b) : "memory");
+    } while (v != (unsigned)(nlg - 1));
+  }
+  __syncthreads();
+  } else {
   if (threadIdx.x == 0) {
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ws_ticket + b) : "memory");
@@ -135,6 +156,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   }
   __syncthreads();
   if (!ticket_last) return;
+  }
   if (threadIdx.x == 0) TL(2);
   if (p.stop_after == 1) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
 
@@ -274,6 +296,9 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     prefer_max_smem(kfn);                                                                        \
+    int per_sm = 0;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);                      \
+    p.designated_tail = (int64_t)grid.x * grid.y <= (int64_t)per_sm * num_sms();                \
     kfn<<<grid, 256, smem, s>>>(p);                                                              \
   } while (0)
 #define ZOOMR_FS_G(DD)               \

@@ -9,16 +9,6 @@ namespace zoomr {
 
 constexpr int kHistBins = 2048;  // vote histogram bins of the top-c threshold search
 
-// (debug) per-phase global timestamps, read back by zoomr_debug_timestamps
-static __device__ unsigned long long g_dbg_ts[2][16];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TS(slot, k) \
-  if (threadIdx.x == 0) g_dbg_ts[slot][k] = gtimer();
-
 // Carves 16-byte-aligned sub-arrays out of dynamic shared memory.
 struct SmemCarve {
   unsigned char *p;

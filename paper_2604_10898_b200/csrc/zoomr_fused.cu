@@ -319,6 +319,3 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   return launch_status();
 }
 
-extern "C" int zoomr_debug_timestamps(unsigned long long *out) {
-  return cudaMemcpyFromSymbol(out, zoomr::g_dbg_ts, sizeof(zoomr::g_dbg_ts)) == cudaSuccess ? 0 : 8;
-}

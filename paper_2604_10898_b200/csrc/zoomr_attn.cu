@@ -627,8 +627,16 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     return p.ws_part + part_slot(ph, w, b, seg) * SLOT;
   };
 
-  auto flush = [&](int ph, int b, int seg) {
+  auto flush = [&](int ph, int b, int seg, bool at_end) {
     TLW_ADD(gw, 7, 1);
+    // At the warp's last flush: if every other part of the segment has already
+    // arrived, this part is the last one -- merge right away, with this part
+    // taken from shared memory, instead of publishing it, fencing and counting
+    // (the counter is read now; its latency hides behind the reductions below).
+    unsigned cnt_seen = 0xffffffffu;
+    if (at_end && bres && npend == 0 && lane == 0)
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cnt_seen)
+                   : "l"(p.ws_cnt + (int64_t)b * LH + seg) : "memory");
     // finish the segment's softmax state and publish it (final or partial)
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -681,8 +689,12 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         if (npend == 0) return;  // else: still count the pending phase-A partials below
       }
     }
-    if (!final_out) {  // partial
-      float *ps = p.ws_part + part_slot(ph, gw, b, seg) * SLOT;
+    cnt_seen = __shfl_sync(0xffffffffu, cnt_seen, 0);
+    const bool shortcut = !final_out && bres && cnt_seen == (unsigned)(n0w + n1w - 1);
+    // the pair's ring is idle at its last flush: stage 0 holds this part for the merge
+    float *own = reinterpret_cast<float *>(smem + pair * kStages * S::STAGE_BYTES);
+    if (!final_out) {  // partial (published, or kept in shared memory for the shortcut)
+      float *ps = shortcut ? own : p.ws_part + part_slot(ph, gw, b, seg) * SLOT;
       if (owner) {
         if (gq == 0) {
           ps[n0] = m0;
@@ -724,11 +736,16 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       seg_parts(xb, xs, wf0, n0w, wf1, n1w);
       const int nparts = n0w + n1w;
       int32_t *cnt = p.ws_cnt + (int64_t)xb * LH + xs;
-      int old = 0;
-      if (lane == 0)
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old != nparts - 1) continue;  // not the last arriving part
+      int own_j = -1;  // index of this warp's part when it is merged from shared memory
+      if (shortcut && it == narr - 1) {
+        own_j = ph ? n0w + (int)(gw - wf1) : (int)(gw - wf0);
+      } else {
+        int old = 0;
+        if (lane == 0)
+          asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old != nparts - 1) continue;  // not the last arriving part
+      }
       const unsigned long long tl_m0 = TL_NOW();
       __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
       // last arriver: online merge of the parts in a fixed order (deterministic),
@@ -752,7 +769,18 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         float4 ov4[NPF][PER];
 #pragma unroll
         for (int j = 0; j < NPF; ++j) {
-          if (j0 + j < nparts) {
+          if (j0 + j == own_j) {  // this warp's part, in shared memory
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              mh[j][h] = own[h];
+              lh[j][h] = own[G + h];
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+              const int f = lane + 32 * u;
+              ov4[j][u] = f < NV4 ? reinterpret_cast<const float4 *>(own + HDR)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          } else if (j0 + j < nparts) {
             const float *qp = part_ptr(xb, xs, j0 + j, wf0, n0w, wf1);
 #pragma unroll
             for (int h = 0; h < G; ++h) {
@@ -839,7 +867,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       tis = wk.tis;
     }
     if (ph != cur_ph || b != cur_b || seg != cur_seg) {
-      if (cur_b >= 0) flush(cur_ph, cur_b, cur_seg);
+      if (cur_b >= 0) flush(cur_ph, cur_b, cur_seg, k >= ntot);
       if (k >= ntot) {
         TL(5);
         TL_CTA(2);

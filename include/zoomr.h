@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 2
+#define ZOOMR_ABI_VERSION 3
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -201,16 +201,52 @@ int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *
  * KV-head-sharded mode (no all-reduce point): use the separate calls there.
  * workspace: >= zoomr_select_workspace_bytes(geom, batch, max_summaries) bytes of
  * device memory, zero-filled once before the first call; every call leaves it
- * ready for the next (its per-sequence tickets are reset). */
+ * ready for the next (its per-sequence tickets are reset).
+ *
+ * close_items entries (b, i) with i < 0 mean "nothing closed" and are skipped
+ * (zoomr_track_segments writes one entry per sequence).  update (nullable,
+ * uint8 [B]): update[b] == 0 keeps sequence b's flags from the last update --
+ * no a2/a3 for it, partial / agreeability untouched -- while a1 and a4 still
+ * run (the selection is refreshed only at semantic boundaries, Alg.1 @P:417;
+ * I_f is rebuilt every step from the held flags, reading Q14). */
 size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t batch, int32_t max_summaries);
 
 int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
                        const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                       const uint8_t *update,
                        float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
                        int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
                        int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
                        int32_t *topk_out, void *workspace, size_t workspace_bytes,
                        int32_t *dev_status, void *stream);
+
+/* ---- Algorithm 1's per-token bookkeeping, on device ----------
+ *
+ * a0 -- KV append, Alg.1 @P:407 ("Append k_t and v_t to KV cache"): writes the
+ * current token's rows k_new / v_new (bf16 [B][L][H_kv][d]) at position
+ * T = seq_len[b] of sequence b (page page_table[b][T / P], slot T % P), then sets
+ * seq_len[b] = T + 1.  Device errors: INDEX_RANGE (no page for T). */
+int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
+                    const void *v_new, int32_t *seq_len, int32_t *dev_status, void *stream);
+
+/* Segment tracking from the token just appended (P:19-21 summary delimiters,
+ * SPEC ingest_token S:36-45; P:109 semantic boundaries).  token_ids[b] is the id
+ * of the token at position pos = seq_len[b] - 1 of sequence b:
+ *   begin_id: a summary opens at pos; the open tail before it becomes the pending R;
+ *   end_id:   the open summary closes: S_i = [open, pos + 1) (both delimiters
+ *             included), R_i = the pending R; bounds[b][i] = (r0, r1, s0, s1),
+ *             num_summaries[b] = i + 1, close_items[b] = (b, i) -- else (b, -1);
+ *   any id in boundary_ids[0..n_boundary): update[b] = 1 (selection update this
+ *             step, for zoomr_select_fused), else 0.
+ * state: int32 [B][4], 16-byte aligned, = (open summary start or -1, open-tail
+ * start, pending R start, pending R end), initialised by the caller to
+ * (-1, N_p, N_p, N_p) after a prompt of N_p tokens.  Device errors:
+ * SEGMENT_ORDER (begin inside an open summary, end without one), CAPACITY
+ * (more than max_summaries summaries). */
+int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
+                         const int32_t *boundary_ids, int32_t n_boundary, const int32_t *seq_len,
+                         int32_t *bounds, int32_t *num_summaries, int32_t max_summaries, int32_t *state,
+                         int32_t *close_items, uint8_t *update, int32_t *dev_status, void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

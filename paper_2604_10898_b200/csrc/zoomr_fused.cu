@@ -61,6 +61,7 @@ struct FusedParams {
   int32_t *status;
   int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
   int32_t designated_tail;  // the grid is resident at once: the last-launched CTA of b runs a3/a4
+  const uint8_t *update;    // nullable: update[b] == 0 keeps b's flags (no a2/a3; a1 and a4 still run)
 };
 
 template <int D, int G>
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     for (int it = 0; it < p.n_items; ++it) {
       if (p.items[2 * it] != b) continue;
       const int i = p.items[2 * it + 1];
-      if (i < 0 || i >= nt) {
+      if (i < 0) continue;  // "nothing closed" entry
+      if (i >= nt) {
         if (threadIdx.x == 0) set_status(p.status, ZOOMR_ERR_INDEX_RANGE);
         continue;
       }
@@ -103,8 +105,9 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     __syncthreads();  // this CTA's own global writes are visible to it after the barrier
   }
 
-  // ---- a2: alpha + per-voter top-k ----------------------------------------------
-  {
+  // ---- a2: alpha + per-voter top-k (only at a selection update) ---------------------
+  const bool upd = !p.update || p.update[b];
+  if (upd) {
     float *qs = reinterpret_cast<float *>(smem_raw);                 // [G][D]
     float *al = qs + G * D;                                          // [G][MS]
     int *sel_i = reinterpret_cast<int *>(al + G * MS);               // [G][k]
@@ -173,15 +176,20 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   if (p.index_phys)
     for (int x = threadIdx.x; x < p.max_pages; x += blockDim.x) pts[x] = p.page_table[(int64_t)b * p.max_pages + x];
   // collect the aggregate (leaving the accumulators zeroed for the next call)
-  // and stage the segment table for a4
+  // and stage the segment table for a4; without an update, the held flags
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
     bds[i] = reinterpret_cast<const int4 *>(bd)[i];
-    v[i] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
-    A[i] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
-    p.ws_votes[(int64_t)b * MS + i] = 0;
-    p.ws_a[(int64_t)b * MS + i] = 0;
+    if (upd) {
+      v[i] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
+      A[i] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
+      p.ws_votes[(int64_t)b * MS + i] = 0;
+      p.ws_a[(int64_t)b * MS + i] = 0;
+    } else {
+      fl[i] = p.flags[(int64_t)b * MS + i];
+    }
   }
   __syncthreads();
+  if (upd) {
   if (p.partial) {
     int64_t *pv = p.partial + (int64_t)b * 2 * MS;
     for (int i = threadIdx.x; i < MS; i += blockDim.x) {
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
   uint8_t *fo = p.flags + (int64_t)b * MS;
   for (int i = threadIdx.x; i < MS; i += blockDim.x) fo[i] = i < nt ? fl[i] : 0;
   __syncthreads();
+  }  // upd
   if (p.stop_after == 3) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
   if (threadIdx.x == 0) TL(4);
   // ---- a4: the index set --------------------------------------------------------------
@@ -234,6 +243,7 @@ extern "C" size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t b
 
 extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
                                   const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                                  const uint8_t *update,
                                   float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
                                   int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
                                   int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
@@ -260,6 +270,7 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   p.max_summaries = seg->max_summaries;
   p.items = close_items;
   p.n_items = n_close;
+  p.update = update;
   p.mean_keys = mean_keys;
   p.top_k = top_k;
   p.c = c;

@@ -1,0 +1,120 @@
+// Algorithm 1's per-token bookkeeping around the hot path,
+// on device so that a whole decode step -- append, segment tracking, selection
+// update at semantic boundaries, attention -- is one CUDA-graph replay:
+//
+//  * zoomr_append_kv     a0: "Append k_t and v_t to KV cache" (Alg.1 @P:407);
+//  * zoomr_track_segments: the summary delimiters (<|begin_of_summary|>,
+//    <|end_of_summary|>, SPEC ingest_token S:36-45) maintain the
+//    segment table, a closed summary is reported for a1 ("if a new summary S_Nt
+//    is complete", Alg.1 @P:408), and a semantic-boundary token (the preset
+//    punctuation list, P:109 / Appendix) requests the selection update
+//    ("if at a semantic boundary", Alg.1 @P:417).
+#include "common.cuh"
+
+namespace zoomr {
+
+// one CTA per (b, layer); threads over (KV head, d/8 chunks): 16-byte copies
+__global__ void append_kv_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                                 __nv_bfloat16 *kpool, __nv_bfloat16 *vpool, int64_t num_pages,
+                                 const int32_t *__restrict__ page_table, int32_t max_pages, int32_t L, int32_t Hkv,
+                                 int32_t P, int32_t d, const int32_t *__restrict__ seq_len_in, int32_t *status) {
+  const int b = blockIdx.y, l = blockIdx.x;
+  const int T = seq_len_in[b];
+  const int lp = T / P;
+  int page = (T >= 0 && lp < max_pages) ? page_table[(int64_t)b * max_pages + lp] : -1;
+  if (page < 0 || page >= num_pages) {
+    if (threadIdx.x == 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
+    return;
+  }
+  const int cpr = d / 8;  // 16-byte chunks per row
+  for (int x = threadIdx.x; x < Hkv * cpr; x += blockDim.x) {
+    const int g = x / cpr, c = x - g * cpr;
+    const int64_t src = (((int64_t)b * L + l) * Hkv + g) * cpr + c;
+    const int64_t dst = (((((int64_t)l * num_pages + page) * Hkv + g) * P + (T - lp * P)) * d) / 8 + c;
+    reinterpret_cast<uint4 *>(kpool)[dst] = k_new[src];
+    reinterpret_cast<uint4 *>(vpool)[dst] = v_new[src];
+  }
+}
+
+__global__ void advance_kernel(int32_t *seq_len, int32_t batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) seq_len[b] += 1;
+}
+
+// one thread per sequence
+__global__ void track_kernel(int32_t batch, const int32_t *__restrict__ token_ids, int32_t begin_id, int32_t end_id,
+                             const int32_t *__restrict__ boundary_ids, int32_t n_boundary,
+                             const int32_t *__restrict__ seq_len, int32_t *bounds, int32_t *num_summaries,
+                             int32_t max_summaries, int4 *state, int32_t *close_items, uint8_t *update,
+                             int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int tok = token_ids[b];
+  const int pos = seq_len[b] - 1;  // the token just appended
+  int4 st = state[b];              // (open summary start or -1, open-tail start, pending R start, pending R end)
+  int closed = -1;
+  if (tok == begin_id) {
+    if (st.x >= 0) set_status(status, ZOOMR_ERR_SEGMENT_ORDER);  // begin inside an open summary
+    else {
+      st.z = st.y;  // the open tail before the delimiter becomes the pending R
+      st.w = pos;
+      st.x = pos;
+    }
+  } else if (tok == end_id) {
+    if (st.x < 0) set_status(status, ZOOMR_ERR_SEGMENT_ORDER);  // end without an open summary
+    else {
+      const int i = num_summaries[b];
+      if (i >= max_summaries) set_status(status, ZOOMR_ERR_CAPACITY);
+      else {
+        int32_t *bd = bounds + ((int64_t)b * max_summaries + i) * 4;
+        bd[0] = st.z;
+        bd[1] = st.w;
+        bd[2] = st.x;
+        bd[3] = pos + 1;  // delimiters included
+        num_summaries[b] = i + 1;
+        closed = i;
+      }
+      st.x = -1;
+      st.y = pos + 1;
+    }
+  }
+  state[b] = st;
+  close_items[2 * b] = b;
+  close_items[2 * b + 1] = closed;
+  bool bnd = false;
+  for (int j = 0; j < n_boundary; ++j) bnd |= tok == boundary_ids[j];
+  update[b] = bnd ? 1 : 0;
+}
+
+}  // namespace zoomr
+
+using namespace zoomr;
+
+extern "C" int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
+                               const void *v_new, int32_t *seq_len, int32_t *dev_status, void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !kv || !kv->k || !kv->v || !kv->page_table || !k_new || !v_new || !seq_len ||
+      kv->num_pages < 1 || kv->max_pages < 1)
+    return ZOOMR_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  append_kv_kernel<<<dim3(geom->num_layers, batch), 128, 0, s>>>(
+      (const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k, (__nv_bfloat16 *)kv->v, kv->num_pages,
+      kv->page_table, kv->max_pages, geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, seq_len,
+      dev_status);
+  advance_kernel<<<(batch + 127) / 128, 128, 0, s>>>(seq_len, batch);
+  return launch_status();
+}
+
+extern "C" int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
+                                    const int32_t *boundary_ids, int32_t n_boundary, const int32_t *seq_len,
+                                    int32_t *bounds, int32_t *num_summaries, int32_t max_summaries, int32_t *state,
+                                    int32_t *close_items, uint8_t *update, int32_t *dev_status, void *stream) {
+  if (batch < 1 || !token_ids || (n_boundary > 0 && !boundary_ids) || n_boundary < 0 || !seq_len || !bounds ||
+      !num_summaries || max_summaries < 1 || !state || !close_items || !update)
+    return ZOOMR_ERR_INVALID_ARG;
+  track_kernel<<<(batch + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+      batch, token_ids, begin_id, end_id, boundary_ids, n_boundary, seq_len, bounds, num_summaries, max_summaries,
+      reinterpret_cast<int4 *>(state), close_items, update, dev_status);
+  return launch_status();
+}

@@ -23,7 +23,8 @@ A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
 
 EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
            "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
-           "zoomr_select_fused", "zoomr_status_str", "zoomr_abi_version")
+           "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_status_str",
+           "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -47,7 +48,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 2  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 3  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -70,9 +71,13 @@ def lib():
                                                vp, vp]
         L.zoomr_select_workspace_bytes.argtypes = [vp, i32, i32]
         L.zoomr_select_workspace_bytes.restype = sz
-        L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp,
-                                         vp, vp, i32, vp, vp, vp, vp, sz, vp, vp]
+        L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp,
+                                         vp, vp, vp, i32, vp, vp, vp, vp, sz, vp, vp]
         L.zoomr_select_fused.restype = C.c_int
+        L.zoomr_append_kv.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.zoomr_append_kv.restype = C.c_int
+        L.zoomr_track_segments.argtypes = [i32, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp]
+        L.zoomr_track_segments.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -222,14 +227,15 @@ def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:
 def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summaries, seq_len, close_items,
                  mean_keys, top_k, c, sink, window, flags, index, index_count, workspace, partial=None,
                  agreeability=None, alpha_out=None, topk_out=None, dev_status=None, stream=None,
-                 index_phys=None):
-    """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None."""
+                 index_phys=None, update=None):
+    """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None
+    (entries with i < 0 are skipped); update: uint8 [B] or None (0 = keep the flags)."""
     g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
     n_close = 0 if close_items is None else close_items.shape[0]
     rc = lib().zoomr_select_fused(
         C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv), C.byref(sg),
         _ptr(close_items, torch.int32, "close_items") if n_close else None, n_close,
-        _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k), int(c), int(sink), int(window),
+        _ptr(update, torch.uint8, "update"), _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k), int(c), int(sink), int(window),
         _ptr(partial, torch.int64, "partial"), _ptr(flags, torch.uint8, "flags"),
         _ptr(agreeability, torch.float32, "agreeability"), _ptr(index, torch.int32, "index"),
         _ptr(index_phys, torch.int32, "index_phys"), index.shape[1],
@@ -238,3 +244,25 @@ def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summar
         workspace.numel() * workspace.element_size(), _ptr(dev_status, torch.int32, "dev_status"),
         _stream(stream))
     _check("zoomr_select_fused", rc)
+
+
+def append_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_len, dev_status=None, stream=None):
+    """a0 (zoomr_append_kv): rows k_new / v_new bf16 [B][L][H_kv][d] at position seq_len[b]; seq_len += 1."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    rc = lib().zoomr_append_kv(C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"),
+                               _ptr(v_new, torch.bfloat16, "v_new"), _ptr(seq_len, torch.int32, "seq_len"),
+                               _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_append_kv", rc)
+
+
+def track_segments(token_ids, begin_id, end_id, boundary_ids, seq_len, bounds, num_summaries, state,
+                   close_items, update, dev_status=None, stream=None):
+    """zoomr_track_segments: summary delimiters / semantic boundaries of the token just appended."""
+    nb = 0 if boundary_ids is None else boundary_ids.numel()
+    rc = lib().zoomr_track_segments(
+        token_ids.shape[0], _ptr(token_ids, torch.int32, "token_ids"), int(begin_id), int(end_id),
+        _ptr(boundary_ids, torch.int32, "boundary_ids") if nb else None, nb, _ptr(seq_len, torch.int32, "seq_len"),
+        _ptr(bounds, torch.int32, "bounds"), _ptr(num_summaries, torch.int32, "num_summaries"), bounds.shape[1],
+        _ptr(state, torch.int32, "state"), _ptr(close_items, torch.int32, "close_items"),
+        _ptr(update, torch.uint8, "update"), _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_track_segments", rc)

@@ -179,6 +179,18 @@ class DecodeLoop(ZoomrStep):
         self.flags.zero_()
         self.track_state.copy_(torch.stack([torch.full_like(n, -1), n, n, n], dim=1))
 
+    def start_from(self, bounds, num_summaries, seq_len):
+        """Continue an existing context: its segment table, N_t and T (device tensors); the
+        open tail starts after the last closed summary.  Mean keys must already be cached."""
+        self.bounds.copy_(bounds)
+        self.num_summaries.copy_(num_summaries)
+        self.seq_len.copy_(seq_len)
+        self.flags.zero_()
+        last = torch.clamp(num_summaries.long() - 1, min=0)
+        tail = torch.where(num_summaries > 0, bounds[torch.arange(self.batch, device=bounds.device), last, 3],
+                           torch.zeros_like(num_summaries))
+        self.track_state.copy_(torch.stack([torch.full_like(tail, -1), tail, tail, tail], dim=1))
+
     def decode_step(self, kv, k_new, v_new, q, token_ids):
         """Enqueue one step; k_new/v_new bf16 [B][L][H_kv][d], q bf16 [B][L][H_q][d], token_ids int32 [B]."""
         k_pool, v_pool, page_table = kv

@@ -377,6 +377,34 @@ def run_ours(args):
         decode_loop = {"us_per_token": us, "tokens": n_tok, "selection_updates": sum(t == 200 for t in toks),
                        "launches_per_token": 5, "note": "append + segment tracking + fused select (a2/a3 at "
                        "sentence boundaries only) + a5; the 256 steps captured in one CUDA graph"}
+    # the paper's comparison policies on the same kernels (NEXT-3), informational:
+    # StreamingLLM at ZoomR's budget (mean |I_f|), SumR (all summaries kept); a4 + a5 per step
+    policies = None
+    if world == 1 and not args.no_loop:
+        from paper_2604_10898_b200.policies import PolicyStep
+        budget = int(round(sum(sum(c) for c in counts) / sum(len(c) for c in counts)))
+        policies = {}
+        for pol in ("streamingllm", "sumr"):
+            gs, cnt_pol = [], []
+            for s_ in sets:
+                ps = PolicyStep(pol, shape, Bseq, s_["inp"].bounds.shape[1], cfg.T, prm, budget=budget)
+                ps.prepare(s_["inp"].num_summaries)
+                gp = ps.capture(s_["inp"].q, s_["kv"], s_["seg"], update_selection=False)
+                gs.append((gp, ps))
+            for i in range(W):
+                gs[i % R][0].replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(K):
+                gs[i % R][0].replay()
+            e1.record()
+            torch.cuda.synchronize()
+            for gp, ps in gs:
+                ps.check_status()
+            policies[pol] = {"us_per_step": e0.elapsed_time(e1) * 1e3 / K,
+                             "index_count_mean": float(sum(int(ps.count.float().mean()) for _, ps in gs) / R)}
+        policies["budget"] = budget
     # per-stage breakdown (informational): each stage alone, graph-replayed
     stages = {}
     s0 = sets[0]
@@ -443,6 +471,7 @@ def run_ours(args):
                      "launch_us": attn_s * 1e6},
         "stages_us": stages,
         "decode_loop": decode_loop,
+        "policies": policies,
         "e2e": {"value": world * Bseq * K / t_e2e, "unit": "seqs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": sum(full_launch if is_full(i) else light_launch for i in range(K)),

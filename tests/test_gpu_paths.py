@@ -109,3 +109,44 @@ def test_device_status_codes():
                                                                                  device="cuda"))
     torch.cuda.synchronize()
     assert int(st2.status.item()) == Z.ERR_EMPTY_SEGMENT
+
+
+@pytest.mark.parametrize("policy", ["streamingllm", "sumr"])
+@pytest.mark.parametrize("cfg_name", ["tiny", "8b16k"])
+def test_comparison_policies(policy, cfg_name):
+    """StreamingLLM at a matched budget and SumR on the same kernels (a4 with fixed
+    flags + a5) vs the oracle's index build and attention on the same flags."""
+    import numpy as np
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.policies import PolicyStep
+    from paper_2604_10898_b200.step import StepParams
+    cfg = S.CONFIGS[cfg_name]
+    inp = S.generate(cfg, device="cuda", seed=4)
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    budget = 2 * cfg.window
+    st = PolicyStep(policy, shape, 1, inp.bounds.shape[1], cfg.T, StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window),
+                    budget=budget)
+    st.prepare(inp.num_summaries)
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st.run(inp.q, kv, seg)
+    torch.cuda.synchronize()
+    st.check_status()
+    sg = PY.seg_host(inp, 0)
+    flags = np.ones(len(sg), np.uint8) if policy == "sumr" else np.zeros(len(sg), np.uint8)
+    idx = oracle.build_index(sg, flags, cfg.T, st.params.sink, st.params.window)
+    cnt = int(st.count[0])
+    assert cnt == len(idx) and np.array_equal(st.index[0, :cnt].cpu().numpy(), idx)
+    if policy == "streamingllm":
+        assert cnt == min(budget, cfg.T)
+    layers, heads = ([0], [0, cfg.Hq - 1]) if cfg_name == "8b16k" else (range(cfg.L), range(cfg.Hq))
+    q = PY.bf16_bits(inp.q[0])
+    out = st.out[0].cpu().numpy().astype(np.float64)
+    G = cfg.Hq // cfg.Hkv
+    for l in layers:
+        Kr = PY.gather_tokens(inp, 0, idx, "k", layers=[l])
+        Vr = PY.gather_tokens(inp, 0, idx, "v", layers=[l])
+        for h in heads:
+            o = oracle.attend_one(q[l, h], np.ascontiguousarray(Kr[:, 0, h // G]), np.ascontiguousarray(Vr[:, 0, h // G]),
+                                  np.arange(len(idx)))
+            assert np.abs(out[l, h] - o).max() <= 2e-3

@@ -72,7 +72,7 @@ struct AttnShape {
 };
 
 struct TmaMaps {
-  CUtensorMap k16, k8, v16, v8;  // 2D [total rows][D] views of the pools, boxes of 16 / 8 rows
+  CUtensorMap k32, k16, k8, v32, v16, v8;  // 2D [total rows][D] views of the pools, boxes of 32 / 16 / 8 rows
 };
 
 struct AttnParams {
@@ -507,11 +507,15 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       const int pos = lane - rs, len = re - rs;
       const int n16 = (len >> 4) << 4, n8 = ((len & 15) >> 3) << 3;
       // TMA boxes need 128-byte aligned destinations: d >= 64 only (d < 64 configs are toy-sized)
-      const bool lead16 = S::SWZ && cok && pos < n16 && (pos & 15) == 0;
-      const bool lead8 = S::SWZ && cok && n8 && pos == n16;
+      // a whole tile that is one run (a window or zoomed stretch inside one page): one 32-row box
+      const bool whole = S::SWZ && len == 32;
+      const bool lead32 = whole && cok && pos == 0;
+      const bool lead16 = S::SWZ && !whole && cok && pos < n16 && (pos & 15) == 0;
+      const bool lead8 = S::SWZ && !whole && cok && n8 && pos == n16;
       const bool byhand = !cok || !S::SWZ || pos >= n16 + n8;
       const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8);
-      const uint32_t tx = (uint32_t)((__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
+      const uint32_t tx = (uint32_t)((__ballot_sync(0xffffffffu, lead32) ? 32 : 0) * S::RB * 2 +
+                                     (__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
       const int s = (int)(k % kStages);
       mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1), 6000000 + (int)k);
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
@@ -521,6 +525,14 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       __syncwarp();
       // one issue block per box height: the tensor map (like the barrier and the
       // stage) is warp-uniform, so only the row and the destination vary per lane
+      if (lead32) {
+#pragma unroll
+        for (int rg = 0; rg < S::NREG; ++rg) {
+          const uint32_t off = (uint32_t)(rg * S::REG_BYTES);
+          tma_load_2d(stK + off, &maps.k32, rg * S::BX, grow, &fullp[s]);
+          tma_load_2d(stV + off, &maps.v32, rg * S::BX, grow, &fullp[s]);
+        }
+      }
       if (lead16) {
 #pragma unroll
         for (int rg = 0; rg < S::NREG; ++rg) {
@@ -1115,7 +1127,8 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     const uint64_t rows = (uint64_t)geom->num_layers * kv->num_pages * geom->num_kv_heads * geom->page_size;
     if (rows >= (1ull << 31)) return ZOOMR_ERR_UNSUPPORTED;  // TMA row coordinate is int32
     const int d = geom->head_dim;
-    if (encode_pool_map(&maps.k16, kv->k, d, rows, 16) || encode_pool_map(&maps.k8, kv->k, d, rows, 8) ||
+    if (encode_pool_map(&maps.k32, kv->k, d, rows, 32) || encode_pool_map(&maps.v32, kv->v, d, rows, 32) ||
+        encode_pool_map(&maps.k16, kv->k, d, rows, 16) || encode_pool_map(&maps.k8, kv->k, d, rows, 8) ||
         encode_pool_map(&maps.v16, kv->v, d, rows, 16) || encode_pool_map(&maps.v8, kv->v, d, rows, 8))
       return ZOOMR_ERR_CUDA;
   }

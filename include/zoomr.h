@@ -51,7 +51,7 @@ extern "C" {
 typedef enum {
   ZOOMR_OK = 0,
   ZOOMR_ERR_INVALID_ARG = 1,   /* NULL pointer, negative size, top_k < 1, c < 0, ...     */
-  ZOOMR_ERR_DIM_MISMATCH = 2,  /* H_q % H_kv != 0, G = H_q/H_kv not in {1, 2, 4, 8}       */
+  ZOOMR_ERR_DIM_MISMATCH = 2,  /* H_q % H_kv != 0, G = H_q/H_kv not in {1, 2, 4, 7, 8}    */
   ZOOMR_ERR_EMPTY_SEGMENT = 3, /* device: s1 <= s0 (SPEC EmptySegment)             */
   ZOOMR_ERR_SEGMENT_ORDER = 4, /* device: r0<=r1<=s0<s1<=next r0 violated        */
   ZOOMR_ERR_INDEX_RANGE = 5,   /* device: s1 > T, N_t > max_summaries, page beyond table  */
@@ -72,7 +72,7 @@ typedef enum {
 typedef struct {
   int32_t num_layers;   /* N_L                                    */
   int32_t num_q_heads;  /* H_q                                            */
-  int32_t num_kv_heads; /* H_kv; G = H_q / H_kv in {1, 2, 4, 8}            */
+  int32_t num_kv_heads; /* H_kv; G = H_q / H_kv in {1, 2, 4, 7, 8}         */
   int32_t head_dim;     /* d in {16, 32, 64, 128}                         */
   int32_t page_size;    /* P >= 1 tokens per KV page                      */
 } zoomr_geom;

@@ -92,7 +92,7 @@ inline int check_geom(const zoomr_geom *g) {
   if (!valid_geom(g)) return ZOOMR_ERR_INVALID_ARG;
   if (g->num_q_heads % g->num_kv_heads) return ZOOMR_ERR_DIM_MISMATCH;
   int G = g->num_q_heads / g->num_kv_heads;
-  if (G != 1 && G != 2 && G != 4 && G != 8) return ZOOMR_ERR_DIM_MISMATCH;
+  if (G != 1 && G != 2 && G != 4 && G != 7 && G != 8) return ZOOMR_ERR_DIM_MISMATCH;  // 7: Qwen2.5-7B (28 / 4)
   int d = g->head_dim;
   if (d != 16 && d != 32 && d != 64 && d != 128) return ZOOMR_ERR_UNSUPPORTED;
   return ZOOMR_OK;

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   const int gq = lane >> 2, tq = lane & 3;  // mma fragment row group / thread-in-group
   const int n0 = 2 * tq;                    // the two MMA columns this thread holds: n0, n0+1
   constexpr int NKS = D / 16;               // k-steps of QK^T and m-tiles of O^T
-  constexpr bool kTwoN = (G == 8);          // hi and lo in separate n-tiles
+  constexpr bool kTwoN = (G > 4);           // hi and lo in separate n-tiles (G = 7: column 7 is padding)
   // column -> (head, part) for G <= 4: head = n % G, part = n / G (0 hi, 1 lo, >=2 none)
   const int part0 = kTwoN ? 0 : n0 / G, part1 = kTwoN ? 0 : (n0 + 1) / G;
   constexpr int HDR = (2 * G + 3) / 4 * 4;  // m[G], l[G] padded to a 16-byte boundary
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         float v = o[me][x];
-        if constexpr (G == 8) v += o2[me][x];
+        if constexpr (kTwoN) v += o2[me][x];
         else if constexpr (G == 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
         else if constexpr (G == 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
         ov[me][x] = v;
@@ -674,8 +674,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       }
     }
     // owners: threads whose columns are the hi copies of real heads
-    const bool owner = (G == 8) || (G == 4 && tq < 2) || (G <= 2 && tq == 0);
-    const int nh = (G == 1) ? 1 : 2;  // heads held by an owner thread: n0 (and n0+1)
+    const bool owner = kTwoN || (G == 4 && tq < 2) || (G <= 2 && tq == 0);
+    // heads held by an owner thread: n0 (and n0 + 1 when it is a real head)
+    const int nh = (G == 1) ? 1 : (kTwoN && n0 + 1 >= G) ? 1 : 2;
     int64_t wf0, wf1;
     int n0w, n1w;
     bool final_out = false;
@@ -766,7 +767,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       float *ob = p.out + (((int64_t)xb * p.L + xl) * Hq + (int64_t)xg * G) * D;
       constexpr int NV4 = G * D / 4;
       constexpr int PER = (NV4 + 31) / 32;
-      constexpr int NPF = G >= 8 ? 2 : 4;
+      constexpr int NPF = G > 4 ? 2 : 4;
       float Mh[G], Lh[G];
       float4 acc[PER];
 #pragma unroll
@@ -1146,6 +1147,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
     case 1: ZOOMR_AT(DD, 1); break;  \
     case 2: ZOOMR_AT(DD, 2); break;  \
     case 4: ZOOMR_AT(DD, 4); break;  \
+    case 7: ZOOMR_AT(DD, 7); break;  \
     default: ZOOMR_AT(DD, 8); break; \
   }
   switch (geom->head_dim) {

@@ -317,6 +317,7 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
     case 1: ZOOMR_FS(DD, 1); break;  \
     case 2: ZOOMR_FS(DD, 2); break;  \
     case 4: ZOOMR_FS(DD, 4); break;  \
+    case 7: ZOOMR_FS(DD, 7); break;  \
     default: ZOOMR_FS(DD, 8); break; \
   }
   switch (geom->head_dim) {

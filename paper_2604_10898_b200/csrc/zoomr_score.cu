@@ -99,6 +99,7 @@ extern "C" int zoomr_score(const zoomr_geom *geom, int32_t batch, const void *q,
     case 1: ZOOMR_SC(DD, 1); break;        \
     case 2: ZOOMR_SC(DD, 2); break;        \
     case 4: ZOOMR_SC(DD, 4); break;        \
+    case 7: ZOOMR_SC(DD, 7); break;        \
     default: ZOOMR_SC(DD, 8); break;       \
   }
   switch (D) {

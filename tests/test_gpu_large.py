@@ -132,3 +132,12 @@ def test_update_interval_holds_flags():
     idx_ref = oracle.build_index(seg_h, flags[0, :len(seg_h)].cpu().numpy(), cfg.T - 7, cfg.sink, cfg.window)
     cnt = int(st.count[0])
     assert np.array_equal(st.index[0, :cnt].cpu().numpy(), idx_ref)
+
+
+def test_qwen_shape_g7_full_size_sampled():
+    """NEXT-4: the Qwen2.5-7B grouping (28 query / 4 KV heads, G = 7) at 16K, full size."""
+    inp = S.generate(S.CONFIGS["qwen7b16k"], device="cuda")
+    st = _run(inp, capacity=8192)
+    rep = {}
+    PY.check_sequence_sampled(inp, st, 0, rep, layers=[0, 27], qheads=[0, 6, 7, 27])
+    print(rep)

@@ -36,6 +36,7 @@ def _small(name, **kw):
     _small("d128_g1", d=128, Hq=2, Hkv=2),             # G = 1
     _small("d128_g8", d=128, Hq=16, Hkv=2),            # G = 8 (hi and lo in separate MMA n-tiles)
     _small("d32_g2", d=32, Hq=4, Hkv=2, batch=3),      # d = 32: rows by cp.async only
+    _small("d128_g7", d=128, Hq=14, Hkv=2),            # G = 7 (Qwen2.5-7B grouping; MMA column 7 padded)
 ], ids=lambda c: c.name)
 @pytest.mark.parametrize("fused", [False, True])
 def test_head_dims_and_groups(cfg, fused):

@@ -77,6 +77,9 @@ CONFIGS = {
     # configs[2]: same shape, 32K, batch 64 (batch-sharded)
     "8b32k": Config("8b32k", L=32, Hq=32, Hkv=8, d=128, T=32768, n_pairs=119, LR=250, LS=20, sink=4,
                     window=512, c=4, top_k=2, batch=64, seed=3),
+    # Qwen2.5-7B shape (28 layers, 28 query / 4 KV heads: G = 7), 16K, batch 1
+    "qwen7b16k": Config("qwen7b16k", L=28, Hq=28, Hkv=4, d=128, T=16384, n_pairs=120, LR=116, LS=16, sink=4,
+                        window=512, c=4, top_k=2, seed=6),
     # configs[3]: Llama-3-70B shape, 64K, batch 1 (KV-head-sharded over 8 GPUs)
     "70b64k": Config("70b64k", L=80, Hq=64, Hkv=8, d=128, T=65536, n_pairs=240, LR=250, LS=20,
                      sink=4, window=512, c=4, top_k=2, seed=4),

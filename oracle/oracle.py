@@ -191,6 +191,19 @@ def sparse_decode_attn(q, keys, values, index, L, Hq, Hkv, d, scale=None, thread
     return out
 
 
+def log_partition(q, keys, index, L, Hq, Hkv, d, scale=None):
+    """O8: lse [L][Hq] = ln sum_{j in index} exp(q.k_j * scale). keys uint16 [T][L][Hkv][d]."""
+    q, keys = _u16(q), _u16(keys)
+    index = _i32(index)
+    lse = np.zeros((L, Hq), dtype=np.float64)
+    sc = 1.0 / np.sqrt(d) if scale is None else float(scale)
+    g = _geom(L, Hq, Hkv, d)
+    _check("zo_log_partition", lib().zo_log_partition(
+        C.byref(g), _p(q), _p(keys), C.c_int32(keys.shape[0]), _p(index), C.c_int32(len(index)),
+        C.c_double(sc), _p(lse)))
+    return lse
+
+
 def step(q, keys, values, seg, L, Hq, Hkv, d, top_k, c, sink, window, threads=0):
     """O1..O7 for one sequence (Alg.1 order). Returns a dict of every intermediate."""
     q, keys, values = _u16(q), _u16(keys), _u16(values)

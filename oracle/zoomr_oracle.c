@@ -284,6 +284,38 @@ int zo_sparse_decode_attn(const zo_geom *g, const uint16_t *q, const uint16_t *k
   return rc;
 }
 
+/* ---------------------------------------------- O8 log partition ---- */
+int zo_log_partition(const zo_geom *g, const uint16_t *q, const uint16_t *keys, int32_t T,
+                     const int32_t *index, int32_t count, double scale, double *lse) {
+  if (!g || !q || !keys || !index || !lse || count < 1) return ZO_ERR_INVALID_ARG;
+  const int32_t L = g->num_layers, Hq = g->num_q_heads, Hk = g->num_kv_heads, d = g->head_dim;
+  if (Hk < 1 || Hq % Hk) return ZO_ERR_INVALID_ARG;
+  for (int32_t t = 0; t < count; ++t)
+    if (index[t] < 0 || index[t] >= T) return ZO_ERR_INDEX_RANGE;
+  const int32_t G = Hq / Hk;
+  const int64_t stride = (int64_t)L * Hk * d;
+  for (int32_t lh = 0; lh < L * Hq; ++lh) {
+    const int32_t l = lh / Hq, h = lh % Hq;
+    const uint16_t *qv = q + (int64_t)lh * d;
+    const uint16_t *k0 = keys + ((int64_t)l * Hk + h / G) * d;
+    /* ln sum_j exp(z_j) = m + ln sum_j exp(z_j - m), m = max_j z_j (identical) */
+    double m = -INFINITY;
+    for (int32_t t = 0; t < count; ++t) {
+      double s = 0.0;
+      for (int32_t e = 0; e < d; ++e) s += zo_bf16_to_double(qv[e]) * zo_bf16_to_double(k0[(int64_t)index[t] * stride + e]);
+      if (s * scale > m) m = s * scale;
+    }
+    double sum = 0.0;
+    for (int32_t t = 0; t < count; ++t) {
+      double s = 0.0;
+      for (int32_t e = 0; e < d; ++e) s += zo_bf16_to_double(qv[e]) * zo_bf16_to_double(k0[(int64_t)index[t] * stride + e]);
+      sum += exp(s * scale - m);
+    }
+    lse[lh] = m + log(sum);
+  }
+  return ZO_OK;
+}
+
 /* ------------------------------------------------- the whole step ---- */
 int zo_step(const zo_geom *g, const zo_params *p, const uint16_t *q, const uint16_t *keys,
             const uint16_t *values, int32_t T, const int32_t *seg, int32_t n_sum,

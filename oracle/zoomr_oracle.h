@@ -101,6 +101,13 @@ int zo_sparse_decode_attn(const zo_geom *g, const uint16_t *q, const uint16_t *k
                           const uint16_t *values, int32_t T, const int32_t *index,
                           int32_t count, double scale, double *out, int32_t num_threads);
 
+/* O8  (token-sharded split-K) the softmax normaliser of O7 in log form:
+ *     lse[l][h] = ln sum_{j in index} exp(q.k_j * scale)          (P:148's denominator)
+ * for every (l, h) of one sequence.  Not a step of the paper: it is the quantity by
+ * which attention over disjoint index sets combines into attention over their union. */
+int zo_log_partition(const zo_geom *g, const uint16_t *q, const uint16_t *keys, int32_t T,
+                     const int32_t *index, int32_t count, double scale, double *lse);
+
 /* The whole step O1..O7 for one sequence, as Algorithm 1 orders it. */
 typedef struct {
   int32_t top_k, c, sink, window;

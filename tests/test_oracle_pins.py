@@ -452,3 +452,57 @@ def test_step_planted_relevance_recall():
         r = oracle.step(to_bf16_bits(q), to_bf16_bits(K), to_bf16_bits(K), np.asarray(seg, np.int32),
                         L, Hq, Hk, d, 2, 1, sink, window)
         assert set(range(seg[target][0], seg[target][1])) <= set(r["index"].tolist())
+
+
+# ----------------------------------------------------------------- O8 -----
+# (token-sharded split-K: the softmax normaliser in log form)
+def test_log_partition_closed_forms():
+    # one row: ln e^z = z = q.k * scale, by hand: (1*2 + 3*(-1)) / sqrt(2)
+    q = to_bf16_bits([[[1.0, 3.0]]])
+    k = to_bf16_bits([[[[2.0, -1.0]]]])
+    lse = oracle.log_partition(q, k, [0], 1, 1, 1, 2)
+    assert abs(lse[0, 0] - (-1.0 / math.sqrt(2))) < 1e-15
+    # q = 0: every logit is 0, ln(count)
+    rng = np.random.default_rng(31)
+    K = to_bf16_bits(rng.normal(size=(9, 2, 2, 8)))
+    lse = oracle.log_partition(to_bf16_bits(np.zeros((2, 4, 8))), K, [0, 2, 3, 7, 8], 2, 4, 2, 8)
+    np.testing.assert_allclose(lse, np.full((2, 4), math.log(5)), rtol=0, atol=1e-15)
+    # the same row listed twice: z + ln 2
+    qb = to_bf16_bits(rng.normal(size=(2, 4, 8)))
+    one = oracle.log_partition(qb, K, [4], 2, 4, 2, 8)
+    two = oracle.log_partition(qb, K, [4, 4], 2, 4, 2, 8)
+    np.testing.assert_allclose(two, one + math.log(2), rtol=0, atol=1e-13)
+
+
+def test_log_partition_brute_force_and_gqa():
+    rng = np.random.default_rng(32)
+    T, L, Hq, Hk, d = 15, 2, 4, 2, 8
+    K = to_bf16_bits(rng.normal(size=(T, L, Hk, d)) * 2)
+    q = to_bf16_bits(rng.normal(size=(L, Hq, d)))
+    idx = np.array([0, 3, 4, 9, 14])
+    lse = oracle.log_partition(q, K, idx, L, Hq, Hk, d)
+    Kf, qf = bf16_bits_to_float(K).astype(np.float64), bf16_bits_to_float(q).astype(np.float64)
+    for l in range(L):
+        for h in range(Hq):
+            z = [float(np.dot(qf[l, h], Kf[t, l, h // (Hq // Hk)])) / math.sqrt(d) for t in idx]
+            assert abs(lse[l, h] - math.log(sum(math.exp(v) for v in z))) < 1e-12
+
+
+def test_log_partition_combines_attention_over_disjoint_sets():
+    # softmax over I1 u I2 = (e^{lse1} o1 + e^{lse2} o2) / (e^{lse1} + e^{lse2}); ties O8 to O7
+    rng = np.random.default_rng(33)
+    T, d = 30, 16
+    kb = to_bf16_bits(rng.normal(size=(T, 1, 1, d)) * 2)
+    vb = to_bf16_bits(rng.normal(size=(T, 1, 1, d)))
+    qb = to_bf16_bits(rng.normal(size=(1, 1, d)))
+    perm = rng.permutation(T)
+    I1, I2 = np.sort(perm[:11]), np.sort(perm[11:])
+    o1 = oracle.attend_one(qb[0, 0], kb[:, 0, 0], vb[:, 0, 0], I1)
+    o2 = oracle.attend_one(qb[0, 0], kb[:, 0, 0], vb[:, 0, 0], I2)
+    l1 = oracle.log_partition(qb, kb, I1, 1, 1, 1, d)[0, 0]
+    l2 = oracle.log_partition(qb, kb, I2, 1, 1, 1, d)[0, 0]
+    full = oracle.attend_one(qb[0, 0], kb[:, 0, 0], vb[:, 0, 0], np.arange(T))
+    w1, w2 = math.exp(l1), math.exp(l2)
+    np.testing.assert_allclose((w1 * o1 + w2 * o2) / (w1 + w2), full, rtol=0, atol=1e-13)
+    lf = oracle.log_partition(qb, kb, np.arange(T), 1, 1, 1, d)[0, 0]
+    assert abs(lf - math.log(w1 + w2)) < 1e-13

@@ -15,6 +15,9 @@
  *   zoomr_build_index         a4  multi-granularity index I_f    P:69-72, Alg.1 @P:421-422
  *   zoomr_sparse_decode_attn  a5  paged gather + GQA decode
  *                                 attention over I_f
+ * plus the fused select (a1..a4 in one launch), Algorithm 1's per-token
+ * bookkeeping (KV append, segment tracking) and the token-sharded split-K
+ * pieces (index restriction, a5 with log-sum-exp, the merge).
  *
  * Conventions shared by every call
  *  - Ownership: every array argument is DEVICE memory allocated and owned by
@@ -46,7 +49,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 3
+#define ZOOMR_ABI_VERSION 4
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -247,6 +250,50 @@ int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int32_t begin_
                          const int32_t *boundary_ids, int32_t n_boundary, const int32_t *seq_len,
                          int32_t *bounds, int32_t *num_summaries, int32_t max_summaries, int32_t *state,
                          int32_t *close_items, uint8_t *update, int32_t *dev_status, void *stream);
+
+/* ---- Token-sharded split-K across GPUs (H_kv < #GPUs) --------
+ *
+ * The KV cache of a sequence is spread over R ranks by token (owner[b][t] = the
+ * rank holding token t; a rank's page table maps the pages of its tokens).  The
+ * selection (a1..a4) is replicated -- every rank holds the mean keys of every
+ * closed summary -- so every rank derives the same I_f.  Each rank attends over
+ * the part of I_f it owns and the R partial results are combined by their
+ * partition functions: for disjoint I_1 .. I_R with union I_f,
+ *   softmax-attention over I_f = sum_r e^{lse_r} o_r / sum_r e^{lse_r},
+ *   lse_r = ln sum_{j in I_r} exp(s_j),  s_j = q . k_j * softmax_scale.
+ *
+ * zoomr_shard_index: local_index[b*cap + 0 .. local_count[b]) = the entries t of
+ * index[b*cap + 0 .. min(index_count[b], cap)) with owner[b*owner_stride + t] ==
+ * rank, order kept.  owner: uint8 [B][owner_stride] (device).  Device errors:
+ * INDEX_RANGE (t < 0 or t >= owner_stride; the entry is dropped). */
+int zoomr_shard_index(int32_t batch, const int32_t *index, const int32_t *index_count,
+                      int32_t index_capacity, const uint8_t *owner, int32_t owner_stride, int32_t rank,
+                      int32_t *local_index, int32_t *local_count, int32_t *dev_status, void *stream);
+
+/* a5 over an arbitrary (e.g. rank-local) index list, also writing the natural-log
+ * partition function lse: fp32 [B][L][H_q], lse[b,l,h] = ln sum_{j in I_b}
+ * exp(q[b,l,h] . k_j * softmax_scale).  Arguments as zoomr_sparse_decode_attn
+ * without the phase-A rows (seq_len = NULL); lse must be non-NULL.  A sequence
+ * with index_count 0 is skipped: its out and lse rows are left untouched (the
+ * merge below excludes it through part_count). */
+int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
+                                 const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                 const int32_t *index_count, int32_t index_capacity, float softmax_scale,
+                                 float *out, float *lse, void *workspace, size_t workspace_bytes,
+                                 int32_t *dev_status, void *stream);
+
+/* Combine n_parts partial attention results (normally the all-gathered outputs
+ * of zoomr_sparse_decode_attn_lse on each rank, over disjoint index sets):
+ *   part_out fp32 [n_parts][B][L][H_q][d], part_lse fp32 [n_parts][B][L][H_q],
+ *   part_count int32 [n_parts][B] (nullable): part r of sequence b is skipped
+ *   when part_count[r*B + b] == 0 (its rows are not read).
+ *   out[b,l,h] = sum_r w_r part_out[r,b,l,h] / sum_r w_r,  w_r = exp(lse_r - max_r lse_r),
+ * parts in order r = 0 .. n_parts-1 (deterministic, identical on every rank);
+ * lse (nullable) = the combined partition function.  A sequence with no part
+ * gets out = 0, lse = -inf. */
+int zoomr_merge_attn(const zoomr_geom *geom, int32_t batch, int32_t n_parts, const float *part_out,
+                     const float *part_lse, const int32_t *part_count, float *out, float *lse,
+                     void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

@@ -87,6 +87,7 @@ struct AttnParams {
   const int32_t *count;
   int32_t cap;
   float *out;
+  float *lse;      // nullable: natural-log partition function per (b, l, h) (token-sharded split-K)
   float *ws_part;  // [2][NW + B*L*Hkv][SLOT]: partial of (phase, warp w, segment s) at [phase][w + s]
   int32_t *ws_cnt; // [B*L*Hkv]
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
@@ -698,6 +699,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
               ob[(int64_t)(n0 + 1) * D + e + 8] = ov[me][3] * inv1;
             }
           }
+          if (p.lse && gq == 0) {  // ln sum_j exp(s_j) = (m + log2 l) * ln 2 (scores are in the log2 domain)
+            float *lb = p.lse + ((int64_t)b * p.L + l) * Hq + (int64_t)g * G;
+            lb[n0] = (m0 + log2f(l0)) * 0.6931471805599453f;
+            if (nh == 2) lb[n0 + 1] = (m1 + log2f(l1)) * 0.6931471805599453f;
+          }
         }
         if (npend == 0) return;  // else: still count the pending phase-A partials below
       }
@@ -857,6 +863,11 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
           reinterpret_cast<float4 *>(ob)[f] =
               make_float4(acc[u].x * inv, acc[u].y * inv, acc[u].z * inv, acc[u].w * inv);
         }
+      }
+      if (p.lse && lane == 0) {
+        float *lb = p.lse + ((int64_t)xb * p.L + xl) * Hq + (int64_t)xg * G;
+#pragma unroll
+        for (int h = 0; h < G; ++h) lb[h] = (Mh[h] + log2f(Lh[h])) * 0.6931471805599453f;
       }
       if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
       TLW_ADD(gw, 2, 1);
@@ -1077,12 +1088,11 @@ extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t bat
   return ((part + 255) / 256) * 256 + cnt;
 }
 
-extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
-                                        const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
-                                        const int32_t *index_count, int32_t index_capacity,
-                                        const int32_t *seq_len, int32_t sink, int32_t window,
-                                        float softmax_scale, float *out, void *workspace,
-                                        size_t workspace_bytes, int32_t *dev_status, void *stream) {
+static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                              const int32_t *index, const int32_t *index_phys, const int32_t *index_count,
+                              int32_t index_capacity, const int32_t *seq_len, int32_t sink, int32_t window,
+                              float softmax_scale, float *out, float *lse, void *workspace, size_t workspace_bytes,
+                              int32_t *dev_status, void *stream) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !q || !kv || !kv->k || !kv->v || !kv->page_table || !index || !index_count ||
@@ -1104,6 +1114,7 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
   prm.count = index_count;
   prm.cap = index_capacity;
   prm.out = out;
+  prm.lse = lse;
   const size_t part = attn_ws_part_floats(geom, batch) * sizeof(float);
   prm.ws_part = (float *)workspace;
   prm.ws_cnt = (int32_t *)((char *)workspace + ((part + 255) / 256) * 256);
@@ -1159,6 +1170,26 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
 #undef ZOOMR_AT_G
 #undef ZOOMR_AT
   return launch_status();
+}
+
+extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
+                                        const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                        const int32_t *index_count, int32_t index_capacity,
+                                        const int32_t *seq_len, int32_t sink, int32_t window,
+                                        float softmax_scale, float *out, void *workspace,
+                                        size_t workspace_bytes, int32_t *dev_status, void *stream) {
+  return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
+                            softmax_scale, out, nullptr, workspace, workspace_bytes, dev_status, stream);
+}
+
+extern "C" int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
+                                            const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                            const int32_t *index_count, int32_t index_capacity, float softmax_scale,
+                                            float *out, float *lse, void *workspace, size_t workspace_bytes,
+                                            int32_t *dev_status, void *stream) {
+  if (!lse) return ZOOMR_ERR_INVALID_ARG;
+  return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, nullptr, 0, 0,
+                            softmax_scale, out, lse, workspace, workspace_bytes, dev_status, stream);
 }
 
 extern "C" const char *zoomr_status_str(int status) {

@@ -17,12 +17,25 @@ to split the work, matching BASELINE.json's configs:
   fixed-point sum of round(alpha * 2^32)), so the reduced value is bit-identical
   to the single-GPU one whatever the reduction order.
 
+* token sharding (H_kv < #GPUs, e.g. Qwen2.5-7B's 4 KV
+  heads on 8 GPUs) -- rank r holds the tokens t with owner[b][t] == r
+  (`token_owner_map`: every summary S_i whole on one rank, because a1 reads
+  all of its key rows; every other token in position chunks, round robin).
+  The mean-key cache is replicated (a1 on the summaries a rank owns, then an
+  all-reduce(SUM) of the cache: every entry has exactly one non-zero
+  contribution, so the sum is exact); a2..a4 run replicated and give every
+  rank the same I_f; a5 runs over the rank's part of I_f with its log-sum-exp
+  (`zoomr_shard_index`, `zoomr_sparse_decode_attn_lse`); one all-gather of
+  (out, lse, count) and `zoomr_merge_attn` give every rank the full output.
+
 Host logic only: the kernels are the libzoomr ones.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Optional
+from typing import Callable, Optional
+
+import numpy as np
 
 import torch
 
@@ -97,3 +110,111 @@ class HeadShardedStep(ZoomrStep):
 
     def run(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=False):
         return super().run(q, kv, seg, update_selection, close_items, allreduce or self._ar, fused=False)
+
+
+# ---------------------------------------------------------------- token sharding --
+def token_owner_map(bounds, num_summaries, world: int, stride: int, chunk: int = 64) -> np.ndarray:
+    """uint8 [B][stride]: the rank that holds each token position.
+
+    A token outside every summary goes to rank (t // chunk) % world; a summary
+    S_i = [s0, s1) goes whole to the rank of its first token, (s0 // chunk) %
+    world, so that a1 finds all of its key rows on one rank.  Stateless in t:
+    a decode step appends token t to the same rank (the rank of an open
+    summary's first token while one is open)."""
+    if not 1 <= world <= 255:
+        raise ValueError("token sharding supports 1..255 ranks")
+    bounds = np.asarray(bounds).reshape(len(num_summaries), -1, 4)
+    B = bounds.shape[0]
+    own = ((np.arange(stride) // chunk) % world).astype(np.uint8)
+    out = np.broadcast_to(own, (B, stride)).copy()
+    for b in range(B):
+        for i in range(int(num_summaries[b])):
+            s0, s1 = int(bounds[b, i, 2]), int(bounds[b, i, 3])
+            out[b, s0:s1] = (s0 // chunk) % world
+    return out
+
+
+def gather_exchange(group=None):
+    """The token-sharded exchange: all-gather (out, lse, count) of every rank."""
+    import torch.distributed as dist
+
+    def _ex(out, lse, count, part_out, part_lse, part_count):
+        dist.all_gather(list(part_out.unbind(0)), out, group=group)
+        dist.all_gather(list(part_lse.unbind(0)), lse, group=group)
+        dist.all_gather(list(part_count.unbind(0)), count, group=group)
+    return _ex
+
+
+def allreduce_mean_keys(group=None):
+    import torch.distributed as dist
+
+    def _ar(mk):
+        dist.all_reduce(mk, op=dist.ReduceOp.SUM, group=group)
+    return _ar
+
+
+class TokenShardedStep(ZoomrStep):
+    """ZoomR step over this rank's tokens (full heads): replicated selection,
+    split-K attention over the rank's part of I_f, one all-gather, the merge."""
+
+    def __init__(self, shape: Z.Shape, rank: int, world: int, batch: int, max_summaries: int,
+                 index_capacity: int, params: StepParams, device="cuda", group=None,
+                 debug_outputs: bool = False,
+                 exchange: Optional[Callable] = None, reduce_mean_keys: Optional[Callable] = None):
+        super().__init__(shape, batch, max_summaries, index_capacity, params, device, debug_outputs,
+                         early_known=False)
+        self.rank, self.world = rank, world
+        dev = self.out.device
+        L, Hq, d = shape.num_layers, shape.num_q_heads, shape.head_dim
+        self.mk_local = torch.zeros_like(self.mean_keys)  # this rank's summaries only, zeros elsewhere
+        self.local_index = torch.zeros_like(self.index)
+        self.local_count = torch.zeros_like(self.count)
+        self.out_local = torch.zeros_like(self.out)
+        self.lse_local = torch.zeros(batch, L, Hq, dtype=torch.float32, device=dev)
+        self.part_out = torch.zeros(world, batch, L, Hq, d, dtype=torch.float32, device=dev)
+        self.part_lse = torch.zeros(world, batch, L, Hq, dtype=torch.float32, device=dev)
+        self.part_count = torch.zeros(world, batch, dtype=torch.int32, device=dev)
+        self.lse = torch.zeros(batch, L, Hq, dtype=torch.float32, device=dev)
+        self._ex = exchange or gather_exchange(group)
+        self._ar_mk = reduce_mean_keys or allreduce_mean_keys(group)
+
+    def update_mean_keys(self, kv, seg, items: Optional[torch.Tensor]):
+        """a1 for the closed summaries this rank owns (items may be empty), then the
+        replication of the cache.  Collective: every rank calls it at every close."""
+        if items is not None and items.numel():
+            k_pool, v_pool, page_table = kv
+            bounds, nsum, seq_len = seg
+            Z.update_mean_keys(self.shape, k_pool, v_pool, page_table, bounds, nsum, seq_len, items,
+                               self.mk_local, self.status)
+        self.mean_keys.copy_(self.mk_local)
+        self._ar_mk(self.mean_keys)
+
+    def run(self, q, kv, seg, owner, update_selection: bool = True):
+        """Enqueue one step (a2..a5, the exchange, the merge); the caller ran
+        update_mean_keys for the summaries closed since the last step."""
+        self.run_local(q, kv, seg, owner, update_selection)
+        return self.combine()
+
+    def run_local(self, q, kv, seg, owner, update_selection: bool = True):
+        """The rank-local part: replicated a2..a4, then a5 over this rank's tokens."""
+        bounds, nsum, seq_len = seg
+        p = self.params
+        if update_selection:
+            Z.score(self.shape, q, self.mean_keys, nsum, p.top_k, self.partial, self.alpha, self.topk,
+                    self.status)
+            Z.select_topc(self.partial, nsum, p.c, self.flags, self.agreeability, self.status)
+        Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count, self.status)
+        self.attend_local(q, kv, owner)
+
+    def combine(self):
+        """The exchange of (out, lse, count) and the merge into self.out / self.lse."""
+        self._ex(self.out_local, self.lse_local, self.local_count, self.part_out, self.part_lse, self.part_count)
+        Z.merge_attn(self.shape, self.part_out, self.part_lse, self.out, part_count=self.part_count, lse=self.lse)
+        return self.out
+
+    def attend_local(self, q, kv, owner):
+        """This rank's part of I_f: restriction + a5 with log-sum-exp."""
+        k_pool, v_pool, page_table = kv
+        Z.shard_index(self.index, self.count, owner, self.rank, self.local_index, self.local_count, self.status)
+        Z.sparse_decode_attn_lse(self.shape, q, k_pool, v_pool, page_table, self.local_index, self.local_count,
+                                 self.out_local, self.lse_local, self.workspace, dev_status=self.status)

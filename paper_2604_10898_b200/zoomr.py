@@ -23,8 +23,8 @@ A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
 
 EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
            "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
-           "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_status_str",
-           "zoomr_abi_version")
+           "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
+           "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -48,7 +48,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 3  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 4  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -78,6 +78,13 @@ def lib():
         L.zoomr_append_kv.restype = C.c_int
         L.zoomr_track_segments.argtypes = [i32, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp]
         L.zoomr_track_segments.restype = C.c_int
+        L.zoomr_shard_index.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp]
+        L.zoomr_shard_index.restype = C.c_int
+        L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, vp, vp, vp, sz,
+                                                   vp, vp]
+        L.zoomr_sparse_decode_attn_lse.restype = C.c_int
+        L.zoomr_merge_attn.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
+        L.zoomr_merge_attn.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -217,6 +224,50 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
                                         workspace.element_size(),
                                         _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_sparse_decode_attn", rc)
+
+
+def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out, lse,
+                           workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None):
+    """a5 over any index list, also writing lse fp32 [B][L][H_q] (zoomr_sparse_decode_attn_lse)."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
+    rc = lib().zoomr_sparse_decode_attn_lse(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
+                                            C.byref(kv), _ptr(index, torch.int32, "index"),
+                                            _ptr(index_phys, torch.int32, "index_phys"),
+                                            _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                            C.c_float(sc), _ptr(out, torch.float32, "out"),
+                                            _ptr(lse, torch.float32, "lse"), _ptr(workspace, None, "workspace"),
+                                            workspace.numel() * workspace.element_size(),
+                                            _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_sparse_decode_attn_lse", rc)
+
+
+def shard_index(index, index_count, owner, rank, local_index, local_count, dev_status=None, stream=None):
+    """I_f restricted to the tokens owned by `rank` (zoomr_shard_index). owner: uint8 [B][stride]."""
+    if local_index.shape != index.shape:
+        raise ValueError("local_index must have index's shape")
+    rc = lib().zoomr_shard_index(index.shape[0], _ptr(index, torch.int32, "index"),
+                                 _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                 _ptr(owner, torch.uint8, "owner"), owner.shape[1], int(rank),
+                                 _ptr(local_index, torch.int32, "local_index"),
+                                 _ptr(local_count, torch.int32, "local_count"),
+                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_shard_index", rc)
+
+
+def merge_attn(shape: Shape, part_out, part_lse, out, part_count=None, lse=None, stream=None):
+    """Combine [R][B][L][H_q][d] partial outputs by their lse [R][B][L][H_q] (zoomr_merge_attn)."""
+    R, B = part_out.shape[0], part_out.shape[1]
+    if part_lse.shape != part_out.shape[:-1] or out.shape != part_out.shape[1:]:
+        raise ValueError("merge_attn: part_out [R][B][L][Hq][d], part_lse [R][B][L][Hq], out [B][L][Hq][d]")
+    if part_count is not None and tuple(part_count.shape) != (R, B):
+        raise ValueError("merge_attn: part_count must be [R][B]")
+    g = shape.c()
+    rc = lib().zoomr_merge_attn(C.byref(g), B, R, _ptr(part_out, torch.float32, "part_out"),
+                                _ptr(part_lse, torch.float32, "part_lse"),
+                                _ptr(part_count, torch.int32, "part_count"), _ptr(out, torch.float32, "out"),
+                                _ptr(lse, torch.float32, "lse"), _stream(stream))
+    _check("zoomr_merge_attn", rc)
 
 
 def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:

@@ -139,3 +139,85 @@ def test_batch_sharded_equals_single_process():
         ref = oracle.step(x["q"], x["K"], x["V"], x["seg"], x["L"], x["Hq"], x["Hk"], x["d"], x["top_k"], x["c"],
                           x["sink"], x["window"])
         np.testing.assert_array_equal(merged[s], ref["out"])
+
+
+def _token_sharded_worker(rank, world, port, out):
+    """Rank r holds only the tokens token_owner_map gives it (the others are NaN
+    here, so reading one would poison the result): a1 on its own summaries,
+    all-reduce(SUM) of the mean-key table, replicated a2..a4, attention and
+    log-partition over its part of I_f, one all-gather, the merge."""
+    from paper_2604_10898_b200.parallel import token_owner_map
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x = _instance()
+    T, L, Hq, Hk, d, seg = x["T"], x["L"], x["Hq"], x["Hk"], x["d"], x["seg"]
+    owner = token_owner_map(seg[None], [len(seg)], world, T, chunk=8)[0]
+    nan = np.uint16(0x7FC0)
+    K = np.where((owner == rank)[:, None, None, None], x["K"], nan).astype(np.uint16)
+    V = np.where((owner == rank)[:, None, None, None], x["V"], nan).astype(np.uint16)
+    mine = [i for i in range(len(seg)) if owner[seg[i, 2]] == rank]
+    assert all(np.all(owner[seg[i, 2]:seg[i, 3]] == rank) for i in mine)  # S_i whole on one rank
+    mk = np.zeros((L, Hk, len(seg), d))
+    if mine:
+        mk[:, :, mine] = oracle.update_mean_keys(K, seg[mine], L, Hk, d)
+    mk_t = torch.from_numpy(mk)
+    dist.all_reduce(mk_t, op=dist.ReduceOp.SUM)
+    sc = oracle.score(x["q"], mk_t.numpy(), x["top_k"], L, Hq, Hk, d)
+    flags, _, _ = oracle.select_topc(sc["votes"], sc["A"], x["c"])
+    idx = oracle.build_index(seg, flags, T, x["sink"], x["window"])
+    local = idx[owner[idx] == rank]
+    o = np.zeros((L, Hq, d))
+    lse = np.full((L, Hq), -np.inf)
+    if len(local):
+        o = oracle.sparse_decode_attn(x["q"], K, V, local, L, Hq, Hk, d)
+        lse = oracle.log_partition(x["q"], K, local, L, Hq, Hk, d)
+    parts_o = [torch.zeros(L, Hq, d, dtype=torch.float64) for _ in range(world)]
+    parts_l = [torch.zeros(L, Hq, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts_o, torch.from_numpy(o))
+    dist.all_gather(parts_l, torch.from_numpy(lse))
+    lm = torch.stack(parts_l)                       # [R][L][Hq]
+    w = torch.exp(lm - lm.max(0).values)            # e^{lse_r - max}; empty parts weigh 0
+    merged = (w[..., None] * torch.stack(parts_o)).sum(0) / w.sum(0)[..., None]
+    out[rank] = (flags, idx, merged.numpy(), len(local))
+    dist.destroy_process_group()
+
+
+def test_token_sharded_step_matches_single_process():
+    world = 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_token_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    x = _instance()
+    ref = oracle.step(x["q"], x["K"], x["V"], x["seg"], x["L"], x["Hq"], x["Hk"], x["d"], x["top_k"], x["c"],
+                      x["sink"], x["window"])
+    assert sum(out[r][3] for r in range(world)) == len(ref["index"])
+    for r in range(world):
+        flags, idx, merged, _ = out[r]
+        np.testing.assert_array_equal(flags, ref["flags"])
+        np.testing.assert_array_equal(idx, ref["index"])
+        np.testing.assert_allclose(merged, ref["out"], atol=1e-12, rtol=0)
+
+
+def test_token_owner_map_keeps_summaries_whole():
+    from paper_2604_10898_b200.parallel import token_owner_map
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        world, chunk = int(rng.integers(1, 9)), int(rng.choice([8, 16, 64]))
+        p, seg = int(rng.integers(0, 40)), []
+        for _ in range(int(rng.integers(0, 12))):
+            r0, r1 = p, p + int(rng.integers(0, 50))
+            s1 = r1 + int(rng.integers(1, 30))
+            seg.append([r0, r1, r1, s1])
+            p = s1
+        T = p + int(rng.integers(1, 100))
+        seg = np.array(seg, np.int32).reshape(-1, 4)
+        own = token_owner_map(seg[None], [len(seg)], world, T + 5, chunk)[0]
+        assert own.max() < world
+        for r0, r1, s0, s1 in seg:
+            assert np.all(own[s0:s1] == own[s0])
+        inside = np.zeros(T + 5, bool)
+        for r0, r1, s0, s1 in seg:
+            inside[s0:s1] = True
+        t = np.arange(T + 5)
+        assert np.all(own[~inside] == (t[~inside] // chunk) % world)

@@ -244,6 +244,70 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------- our arm ----
+def token_shard_section(shape, prm, s0, cfg, K, world_sim=8):
+    import numpy as np
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.parallel import TokenShardedStep, token_owner_map
+    inp, kv, seg = s0["inp"], s0["kv"], s0["seg"]
+    Bseq = inp.q.shape[0]
+    own_np = token_owner_map(inp.bounds.cpu().numpy(), inp.num_summaries.cpu().numpy(), world_sim,
+                             int(inp.seq_len.max()), 64)
+    owner = torch.from_numpy(own_np).cuda()
+    steps = []
+
+    def exchange(out, lse, count, po, pl, pc):
+        for r, t in enumerate(steps):
+            po[r].copy_(t.out_local)
+            pl[r].copy_(t.lse_local)
+            pc[r].copy_(t.local_count)
+    for r in range(world_sim):
+        t = TokenShardedStep(shape, r, world_sim, Bseq, inp.bounds.shape[1], cfg.T, prm, exchange=exchange,
+                             reduce_mean_keys=lambda mk: None)
+        t.mean_keys.copy_(s0["st"].mean_keys)  # the replicated cache
+        steps.append(t)
+    graphs = []
+    for t in steps:
+        t.run_local(inp.q, kv, seg, owner)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            t.run_local(inp.q, kv, seg, owner)
+        graphs.append(g)
+    steps[0].combine()
+    torch.cuda.synchronize()
+    gm = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gm):
+        Z.merge_attn(shape, steps[0].part_out, steps[0].part_lse, steps[0].out, part_count=steps[0].part_count,
+                     lse=steps[0].lse)
+
+    def t_us(g):
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / K
+    per_rank = [t_us(g) for g in graphs]
+    merge = t_us(gm)
+    s0["g"].replay()  # the unsharded step on the same (possibly decode-loop-appended) cache
+    torch.cuda.synchronize()
+    err = float((steps[0].out - s0["st"].out).abs().max())
+    for t in steps:
+        t.check_status()
+    L, Hq, d = cfg.L, cfg.Hq, cfg.d
+    return {"ranks": world_sim, "rank_step_us_max": max(per_rank), "rank_step_us_mean": sum(per_rank) / world_sim,
+            "merge_us": merge, "rank_index_share": [round(int(t.local_count.sum()) / max(1, int(t.count.sum())), 3)
+                                                    for t in steps],
+            "exchange_bytes_per_rank": Bseq * L * Hq * (d + 1) * 4 + Bseq * 4,
+            "max_abs_diff_vs_unsharded": err,
+            "note": "ranks simulated one after another on one GPU; each rank: a2+a3+a4 (replicated) + "
+                    "shard_index + a5 with lse over its part of I_f; NVLink all-gather not included"}
+
+
 def run_ours(args):
     rank, world, local = init_dist(args.gpus)
     import zoomr_synth as S
@@ -405,6 +469,13 @@ def run_ours(args):
             policies[pol] = {"us_per_step": e0.elapsed_time(e1) * 1e3 / K,
                              "index_count_mean": float(sum(int(ps.count.float().mean()) for _, ps in gs) / R)}
         policies["budget"] = budget
+    # token-sharded split-K (NEXT-4), informational: 8 ranks simulated one after
+    # another on this GPU, each rank's local step (replicated a2..a4, its part of
+    # I_f through a5 with log-sum-exp) timed alone, then the merge; the
+    # all-gather of (out, lse, count) between GPUs is not part of these numbers
+    token_sharded = None
+    if world == 1 and not args.no_loop:
+        token_sharded = token_shard_section(shape, prm, sets[0], cfg, K)
     # per-stage breakdown (informational): each stage alone, graph-replayed
     stages = {}
     s0 = sets[0]
@@ -472,6 +543,7 @@ def run_ours(args):
         "stages_us": stages,
         "decode_loop": decode_loop,
         "policies": policies,
+        "token_sharded": token_sharded,
         "e2e": {"value": world * Bseq * K / t_e2e, "unit": "seqs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": sum(full_launch if is_full(i) else light_launch for i in range(K)),

@@ -197,13 +197,17 @@ class TokenShardedStep(ZoomrStep):
 
     def run_local(self, q, kv, seg, owner, update_selection: bool = True):
         """The rank-local part: replicated a2..a4, then a5 over this rank's tokens."""
+        k_pool, v_pool, page_table = kv
         bounds, nsum, seq_len = seg
         p = self.params
-        if update_selection:
-            Z.score(self.shape, q, self.mean_keys, nsum, p.top_k, self.partial, self.alpha, self.topk,
-                    self.status)
-            Z.select_topc(self.partial, nsum, p.c, self.flags, self.agreeability, self.status)
-        Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count, self.status)
+        if update_selection:  # a2..a4 in one launch (no a1: the cache is already replicated)
+            Z.select_fused(self.shape, q, k_pool, v_pool, page_table, bounds, nsum, seq_len, None,
+                           self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags, self.index, self.count,
+                           self.sel_workspace, partial=self.partial, agreeability=self.agreeability,
+                           alpha_out=self.alpha, topk_out=self.topk, dev_status=self.status)
+        else:
+            Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count,
+                          self.status)
         self.attend_local(q, kv, owner)
 
     def combine(self):

@@ -204,6 +204,32 @@ def log_partition(q, keys, index, L, Hq, Hkv, d, scale=None):
     return lse
 
 
+def h2o_weights(q, keys, index, L, Hq, Hkv, d, scale=None):
+    """O9: per-retained-token softmax weight averaged over (l, h): fp64 [count]."""
+    q, keys = _u16(q), _u16(keys)
+    index = _i32(index)
+    w = np.zeros(max(len(index), 1), dtype=np.float64)
+    sc = 1.0 / np.sqrt(d) if scale is None else float(scale)
+    g = _geom(L, Hq, Hkv, d)
+    _check("zo_h2o_weights", lib().zo_h2o_weights(
+        C.byref(g), _p(q), _p(keys), C.c_int32(keys.shape[0]), _p(index), C.c_int32(len(index)),
+        C.c_double(sc), _p(w)))
+    return w[:len(index)]
+
+
+def h2o_select(prev, score, T, sink, window, budget):
+    """O9: the next retained set (sorted int32) from the previous one and fp64 scores [T]."""
+    n_prev = len(prev)
+    prev = _i32(prev) if n_prev else np.zeros(1, np.int32)
+    score = np.ascontiguousarray(score, dtype=np.float64)
+    out = np.zeros(max(int(T), 1), dtype=np.int32)
+    cnt = C.c_int32(0)
+    _check("zo_h2o_select", lib().zo_h2o_select(
+        _p(prev), C.c_int32(n_prev), _p(score), C.c_int32(T), C.c_int32(sink), C.c_int32(window),
+        C.c_int32(budget), _p(out), C.c_int32(len(out)), C.byref(cnt)))
+    return out[:cnt.value].copy()
+
+
 def step(q, keys, values, seg, L, Hq, Hkv, d, top_k, c, sink, window, threads=0):
     """O1..O7 for one sequence (Alg.1 order). Returns a dict of every intermediate."""
     q, keys, values = _u16(q), _u16(keys), _u16(values)

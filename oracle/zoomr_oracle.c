@@ -316,6 +316,85 @@ int zo_log_partition(const zo_geom *g, const uint16_t *q, const uint16_t *keys, 
   return ZO_OK;
 }
 
+/* --------------------------------------------------------- O9 H2O ---- */
+int zo_h2o_weights(const zo_geom *g, const uint16_t *q, const uint16_t *keys, int32_t T,
+                   const int32_t *index, int32_t count, double scale, double *w) {
+  if (!g || !q || !keys || !index || !w || count < 1) return ZO_ERR_INVALID_ARG;
+  const int32_t L = g->num_layers, Hq = g->num_q_heads, Hk = g->num_kv_heads, d = g->head_dim;
+  if (Hk < 1 || Hq % Hk) return ZO_ERR_INVALID_ARG;
+  for (int32_t t = 0; t < count; ++t)
+    if (index[t] < 0 || index[t] >= T) return ZO_ERR_INDEX_RANGE;
+  const int32_t G = Hq / Hk;
+  const int64_t stride = (int64_t)L * Hk * d;
+  double *z = (double *)malloc(sizeof(double) * (size_t)count);
+  if (!z) return ZO_ERR_INVALID_ARG;
+  for (int32_t t = 0; t < count; ++t) w[t] = 0.0;
+  for (int32_t lh = 0; lh < L * Hq; ++lh) {
+    const int32_t l = lh / Hq, h = lh % Hq;
+    const uint16_t *qv = q + (int64_t)lh * d;
+    const uint16_t *k0 = keys + ((int64_t)l * Hk + h / G) * d;
+    double m = -INFINITY, den = 0.0;
+    for (int32_t t = 0; t < count; ++t) {
+      double s = 0.0;
+      for (int32_t e = 0; e < d; ++e) s += zo_bf16_to_double(qv[e]) * zo_bf16_to_double(k0[(int64_t)index[t] * stride + e]);
+      z[t] = s * scale;
+      if (z[t] > m) m = z[t];
+    }
+    for (int32_t t = 0; t < count; ++t) den += exp(z[t] - m);
+    for (int32_t t = 0; t < count; ++t) w[t] += exp(z[t] - m) / den; /* softmax weight of row t for (l, h) */
+  }
+  for (int32_t t = 0; t < count; ++t) w[t] /= (double)(L * Hq);
+  free(z);
+  return ZO_OK;
+}
+
+typedef struct {
+  double score;
+  int32_t t;
+} zo_st;
+
+static int cmp_score_desc_pos_asc(const void *x, const void *y) {
+  const zo_st *a = (const zo_st *)x, *b = (const zo_st *)y;
+  if (a->score > b->score) return -1;
+  if (a->score < b->score) return 1;
+  return (a->t > b->t) - (a->t < b->t);
+}
+
+int zo_h2o_select(const int32_t *prev, int32_t n_prev, const double *score, int32_t T, int32_t sink,
+                  int32_t window, int32_t budget, int32_t *out, int32_t capacity, int32_t *count) {
+  if ((!prev && n_prev) || !score || !out || !count || T < 1 || sink < 0 || window < 1 || budget < 0)
+    return ZO_ERR_INVALID_ARG;
+  const int32_t sp = sink < T ? sink : T;
+  const int32_t w0 = T - window > sp ? T - window : sp;
+  const int32_t K = budget - (sp + (T - w0)) > 0 ? budget - (sp + (T - w0)) : 0;
+  zo_st *cand = (zo_st *)malloc(sizeof(zo_st) * (size_t)(n_prev > 0 ? n_prev : 1));
+  uint8_t *in = (uint8_t *)calloc((size_t)T, 1);
+  if (!cand || !in) return ZO_ERR_INVALID_ARG;
+  int32_t nc = 0;
+  for (int32_t i = 0; i < n_prev; ++i) {
+    if (prev[i] < 0 || prev[i] >= T) { free(cand); free(in); return ZO_ERR_INDEX_RANGE; }
+    if (prev[i] >= sp && prev[i] < w0) {
+      cand[nc].score = score[prev[i]];
+      cand[nc].t = prev[i];
+      ++nc;
+    }
+  }
+  qsort(cand, (size_t)nc, sizeof(zo_st), cmp_score_desc_pos_asc);
+  for (int32_t t = 0; t < sp; ++t) in[t] = 1;
+  for (int32_t t = w0; t < T; ++t) in[t] = 1;
+  for (int32_t i = 0; i < nc && i < K; ++i) in[cand[i].t] = 1;
+  int32_t n = 0;
+  for (int32_t t = 0; t < T; ++t)
+    if (in[t]) {
+      if (n >= capacity) { free(cand); free(in); return ZO_ERR_CAPACITY; }
+      out[n++] = t;
+    }
+  *count = n;
+  free(cand);
+  free(in);
+  return ZO_OK;
+}
+
 /* ------------------------------------------------- the whole step ---- */
 int zo_step(const zo_geom *g, const zo_params *p, const uint16_t *q, const uint16_t *keys,
             const uint16_t *values, int32_t T, const int32_t *seg, int32_t n_sum,

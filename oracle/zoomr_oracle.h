@@ -108,6 +108,18 @@ int zo_sparse_decode_attn(const zo_geom *g, const uint16_t *q, const uint16_t *k
 int zo_log_partition(const zo_geom *g, const uint16_t *q, const uint16_t *keys, int32_t T,
                      const int32_t *index, int32_t count, double scale, double *lse);
 
+/* O9  H2O, the paper's heavy-hitter baseline (the paper only cites it, the rule is
+ *     SPEC h2o_step S:349-357):
+ *  zo_h2o_weights: w[j] = (1/(L*H_q)) sum_{l,h} softmax_j(q_{l,h}.k_j * scale) over j in index
+ *                  ("per-retained-token softmax weights averaged over heads/layers");
+ *  zo_h2o_select:  the next retained set = [0, min(sink,T)) u [max(that, T-window), T) u the
+ *                  top-(budget - |sink u window|) entries of prev outside them by score desc,
+ *                  ties -> smaller position; sorted ascending into out[0..*count). */
+int zo_h2o_weights(const zo_geom *g, const uint16_t *q, const uint16_t *keys, int32_t T,
+                   const int32_t *index, int32_t count, double scale, double *w);
+int zo_h2o_select(const int32_t *prev, int32_t n_prev, const double *score, int32_t T, int32_t sink,
+                  int32_t window, int32_t budget, int32_t *out, int32_t capacity, int32_t *count);
+
 /* The whole step O1..O7 for one sequence, as Algorithm 1 orders it. */
 typedef struct {
   int32_t top_k, c, sink, window;

@@ -506,3 +506,76 @@ def test_log_partition_combines_attention_over_disjoint_sets():
     np.testing.assert_allclose((w1 * o1 + w2 * o2) / (w1 + w2), full, rtol=0, atol=1e-13)
     lf = oracle.log_partition(qb, kb, np.arange(T), 1, 1, 1, d)[0, 0]
     assert abs(lf - math.log(w1 + w2)) < 1e-13
+
+
+# ----------------------------------------------------------------- O9 -----
+# H2O (rule from SPEC h2o_step S:349-357)
+def test_h2o_select_spec_examples():
+    # scores {0:0.5, 1:0.1, 2:0.4}, window {3,4}, budget 4 -> evict index 1
+    sc = np.array([0.5, 0.1, 0.4, 0.0, 0.0])
+    assert oracle.h2o_select([0, 1, 2, 3, 4], sc, 5, 0, 2, 4).tolist() == [0, 2, 3, 4]
+    # budget >= length -> nothing evicted
+    assert oracle.h2o_select([0, 1, 2, 3, 4], sc, 5, 0, 2, 5).tolist() == [0, 1, 2, 3, 4]
+    assert oracle.h2o_select([0, 1, 2, 3, 4], sc, 5, 0, 2, 50).tolist() == [0, 1, 2, 3, 4]
+    # equal scores at the eviction boundary -> the smaller index is retained
+    sc2 = np.array([0.3, 0.2, 0.2, 0.0, 0.0])
+    assert oracle.h2o_select([0, 1, 2, 3, 4], sc2, 5, 0, 2, 4).tolist() == [0, 1, 3, 4]
+    # the sink is kept whatever its score; evicted tokens never come back
+    sc3 = np.array([0.0, 0.9, 0.1, 0.8, 0.0, 0.0, 0.0])
+    assert oracle.h2o_select([0, 2, 3, 5, 6], sc3, 7, 1, 2, 4).tolist() == [0, 3, 5, 6]
+    # a token leaving the window becomes a candidate with its accumulated score
+    assert oracle.h2o_select([0, 2, 5, 6], np.array([0, 0, 0.1, 0, 0, 0.5, 0, 0]), 8, 1, 2, 4).tolist() == [0, 5, 6, 7]
+
+
+def test_h2o_select_brute_force():
+    rng = np.random.default_rng(41)
+    for _ in range(300):
+        T = int(rng.integers(1, 60))
+        prev = np.sort(rng.choice(T, size=int(rng.integers(0, T + 1)), replace=False))
+        sc = rng.integers(0, 6, size=T) / 4.0  # many exact ties
+        sink, window, budget = int(rng.integers(0, 6)), int(rng.integers(1, 12)), int(rng.integers(0, 40))
+        got = oracle.h2o_select(prev, sc, T, sink, window, budget).tolist()
+        sp = min(sink, T)
+        w0 = max(sp, T - window)
+        fixed = set(range(sp)) | set(range(w0, T))
+        cand = [t for t in prev.tolist() if sp <= t < w0]
+        K = max(0, budget - len(fixed))
+        kept = sorted(cand, key=lambda t: (-sc[t], t))[:K]
+        assert got == sorted(fixed | set(kept))
+
+
+def test_h2o_weights_are_averaged_softmax():
+    rng = np.random.default_rng(42)
+    T, L, Hq, Hk, d = 25, 2, 4, 2, 8
+    K = to_bf16_bits(rng.normal(size=(T, L, Hk, d)) * 2)
+    q = to_bf16_bits(rng.normal(size=(L, Hq, d)))
+    idx = np.sort(rng.choice(T, size=13, replace=False))
+    w = oracle.h2o_weights(q, K, idx, L, Hq, Hk, d)
+    assert abs(w.sum() - 1.0) < 1e-12 and np.all(w > 0)  # each (l, h) softmax sums to 1
+    import torch
+    Kf = torch.from_numpy(bf16_bits_to_float(K).astype(np.float64))
+    qf = torch.from_numpy(bf16_bits_to_float(q).astype(np.float64))
+    ref = torch.zeros(len(idx), dtype=torch.float64)
+    for l in range(L):
+        for h in range(Hq):
+            z = Kf[idx, l, h // (Hq // Hk)] @ qf[l, h] / math.sqrt(d)
+            ref += torch.softmax(z, 0)
+    np.testing.assert_allclose(w, (ref / (L * Hq)).numpy(), rtol=0, atol=1e-14)
+    # q = 0: uniform weights
+    w0 = oracle.h2o_weights(to_bf16_bits(np.zeros((L, Hq, d))), K, idx, L, Hq, Hk, d)
+    np.testing.assert_allclose(w0, np.full(len(idx), 1 / len(idx)), rtol=0, atol=1e-15)
+
+
+def test_h2o_with_full_budget_is_full_attention():
+    # H2O with budget = total length equals full attention exactly
+    rng = np.random.default_rng(43)
+    T, d = 30, 8
+    kb = to_bf16_bits(rng.normal(size=(T, 1, 1, d)))
+    vb = to_bf16_bits(rng.normal(size=(T, 1, 1, d)))
+    qb = to_bf16_bits(rng.normal(size=(1, 1, d)))
+    prev = np.arange(T - 1)  # retained before the newest token
+    idx = oracle.h2o_select(prev, rng.random(T), T, 2, 4, T)
+    assert idx.tolist() == list(range(T))
+    o = oracle.sparse_decode_attn(qb, kb, vb, idx, 1, 1, 1, d)
+    ref = sdpa_fp64(bf16_bits_to_float(qb[0, 0]), bf16_bits_to_float(kb[:, 0, 0]), bf16_bits_to_float(vb[:, 0, 0]))
+    np.testing.assert_allclose(o[0, 0], ref, rtol=0, atol=1e-12)

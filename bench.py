@@ -442,17 +442,21 @@ def run_ours(args):
                        "launches_per_token": 5, "note": "append + segment tracking + fused select (a2/a3 at "
                        "sentence boundaries only) + a5; the 256 steps captured in one CUDA graph"}
     # the paper's comparison policies on the same kernels (NEXT-3), informational:
-    # StreamingLLM at ZoomR's budget (mean |I_f|), SumR (all summaries kept); a4 + a5 per step
+    # StreamingLLM at ZoomR's budget (mean |I_f|), SumR (all summaries kept): a4 + a5 per step;
+    # H2O at the same budget: eviction by cumulative attention + a5 with logits + accumulation
     policies = None
     if world == 1 and not args.no_loop:
         from paper_2604_10898_b200.policies import PolicyStep
         budget = int(round(sum(sum(c) for c in counts) / sum(len(c) for c in counts)))
         policies = {}
-        for pol in ("streamingllm", "sumr"):
+        for pol in ("streamingllm", "sumr", "h2o"):
             gs, cnt_pol = [], []
             for s_ in sets:
-                ps = PolicyStep(pol, shape, Bseq, s_["inp"].bounds.shape[1], cfg.T, prm, budget=budget)
+                ps = PolicyStep(pol, shape, Bseq, s_["inp"].bounds.shape[1], cfg.T, prm, budget=budget,
+                                max_positions=cfg.T)
                 ps.prepare(s_["inp"].num_summaries)
+                if pol == "h2o":
+                    ps.start_h2o(s_["seg"])
                 gp = ps.capture(s_["inp"].q, s_["kv"], s_["seg"], update_selection=False)
                 gs.append((gp, ps))
             for i in range(W):

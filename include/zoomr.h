@@ -16,8 +16,9 @@
  *   zoomr_sparse_decode_attn  a5  paged gather + GQA decode
  *                                 attention over I_f
  * plus the fused select (a1..a4 in one launch), Algorithm 1's per-token
- * bookkeeping (KV append, segment tracking) and the token-sharded split-K
- * pieces (index restriction, a5 with log-sum-exp, the merge).
+ * bookkeeping (KV append, segment tracking), the token-sharded split-K
+ * pieces (index restriction, a5 with log-sum-exp, the merge) and the H2O
+ * comparison policy (a5 with logits, score accumulation, eviction).
  *
  * Conventions shared by every call
  *  - Ownership: every array argument is DEVICE memory allocated and owned by
@@ -49,7 +50,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 4
+#define ZOOMR_ABI_VERSION 5
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -294,6 +295,49 @@ int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const vo
 int zoomr_merge_attn(const zoomr_geom *geom, int32_t batch, int32_t n_parts, const float *part_out,
                      const float *part_lse, const int32_t *part_count, float *out, float *lse,
                      void *stream);
+
+/* ---- H2O, the paper's heavy-hitter comparison policy ----
+ * The paper only cites H2O; the rule is SPEC h2o_step, readings H1-H2
+ * in DESIGN.md 8c.  One H2O step = zoomr_h2o_select (the retained set I for the
+ * current T) -> zoomr_sparse_decode_attn_logits over I -> zoomr_h2o_accumulate.
+ *
+ * a5 over any index list (as zoomr_sparse_decode_attn_lse), also writing the
+ * logits: logits fp32 [B][L][H_q][index_capacity], logits[b,l,h,i] =
+ * q[b,l,h] . k_{index[b,i]} * softmax_scale for i < index_count[b] (other
+ * entries untouched).  lse and logits must be non-NULL. */
+int zoomr_sparse_decode_attn_logits(const zoomr_geom *geom, int32_t batch, const void *q,
+                                    const zoomr_kv *kv, const int32_t *index, const int32_t *index_count,
+                                    int32_t index_capacity, float softmax_scale, float *out, float *lse,
+                                    float *logits, void *workspace, size_t workspace_bytes,
+                                    int32_t *dev_status, void *stream);
+
+/* The attention each retained token received this step, averaged over layers
+ * and query heads ("per-retained-token softmax weights averaged over
+ * heads/layers"), added to its cumulative score:
+ *   score[b*score_stride + index[b,i]] += (1/(L*H_q)) sum_{l,h} exp(logits[b,l,h,i] - lse[b,l,h])
+ * (fixed summation order: deterministic).  score: fp32 [B][score_stride],
+ * score_stride > every position.  index entries must be distinct within a
+ * sequence.  index_copy / count_copy (nullable, [B][index_capacity] / [B]):
+ * receive a copy of the index set -- the prev_index of the next
+ * zoomr_h2o_select.  Device errors: INDEX_RANGE (position >= score_stride). */
+int zoomr_h2o_accumulate(const zoomr_geom *geom, int32_t batch, const int32_t *index,
+                         const int32_t *index_count, int32_t index_capacity, const float *logits,
+                         const float *lse, float *score, int32_t score_stride, int32_t *index_copy,
+                         int32_t *count_copy, int32_t *dev_status, void *stream);
+
+/* The retained set for T = seq_len[b]: with s' = min(sink, T) and
+ * w0 = max(s', T - window),
+ *   index[b] = [0, s') u top-K(prev_index[b] n [s', w0)) u [w0, T),  K = max(0, budget - s' - (T - w0)),
+ * top-K by cumulative score desc, ties -> smaller position; written sorted
+ * ascending (prev_index must be sorted ascending, as this function writes it).
+ * prev_index and index: int32 [B][index_capacity], distinct buffers.  Evicted
+ * positions never return (they are not in prev_index).  Device errors:
+ * CAPACITY (count clamped), INDEX_RANGE, UNSUPPORTED (more than 16384
+ * previously retained positions in [s', w0)). */
+int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *prev_count,
+                     int32_t index_capacity, const float *score, int32_t score_stride,
+                     const int32_t *seq_len, int32_t sink, int32_t window, int32_t budget, int32_t *index,
+                     int32_t *index_count, int32_t *dev_status, void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

@@ -88,6 +88,7 @@ struct AttnParams {
   int32_t cap;
   float *out;
   float *lse;      // nullable: natural-log partition function per (b, l, h) (token-sharded split-K)
+  float *logits;   // kLogits only: s_j = q . k_j * scale per (b, l, h, index position) (H2O)
   float *ws_part;  // [2][NW + B*L*Hkv][SLOT]: partial of (phase, warp w, segment s) at [phase][w + s]
   int32_t *ws_cnt; // [B*L*Hkv]
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
@@ -235,7 +236,7 @@ struct Sched {
 // merged by the last-arriving warp.  Phase-A partials are published before the
 // wait but counted (arrival atomics) only after it, when the phase-B split --
 // and so the number of parts of every segment -- is known.
-template <int D, int G>
+template <int D, int G, bool kLogits = false>
 __global__ void __launch_bounds__(64 * kPairs, 1)
     sparse_attn_kernel(const AttnParams p, const __grid_constant__ TmaMaps maps) {
   using S = AttnShape<D>;
@@ -956,6 +957,24 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       cm0 = fmaxf(cm0, fmaxf(sacc[mt][0], sacc[mt][2]));
       cm1 = fmaxf(cm1, fmaxf(sacc[mt][1], sacc[mt][3]));
     }
+    if constexpr (kLogits) {  // H2O: the logits of the tile's rows (index positions, no early rows)
+      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      float *lg = p.logits + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * p.cap + (int64_t)tis * kTile;
+      const bool c0 = kTwoN ? n0 < G : part0 == 0, c1 = kTwoN ? n0 + 1 < G : part1 == 0;
+      const int h0 = kTwoN ? n0 : n0 % G, h1 = kTwoN ? n0 + 1 : (n0 + 1) % G;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int t0 = mt * 16 + gq, t1 = t0 + 8;
+        if (t0 < nvalid) {
+          if (c0) lg[(int64_t)h0 * p.cap + t0] = sacc[mt][0] * 0.6931471805599453f;
+          if (c1) lg[(int64_t)h1 * p.cap + t0] = sacc[mt][1] * 0.6931471805599453f;
+        }
+        if (t1 < nvalid) {
+          if (c0) lg[(int64_t)h0 * p.cap + t1] = sacc[mt][2] * 0.6931471805599453f;
+          if (c1) lg[(int64_t)h1 * p.cap + t1] = sacc[mt][3] * 0.6931471805599453f;
+        }
+      }
+    }
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
       cm0 = fmaxf(cm0, __shfl_xor_sync(0xffffffffu, cm0, off));
@@ -1092,7 +1111,7 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
                               const int32_t *index, const int32_t *index_phys, const int32_t *index_count,
                               int32_t index_capacity, const int32_t *seq_len, int32_t sink, int32_t window,
                               float softmax_scale, float *out, float *lse, void *workspace, size_t workspace_bytes,
-                              int32_t *dev_status, void *stream) {
+                              int32_t *dev_status, void *stream, float *logits = nullptr) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !q || !kv || !kv->k || !kv->v || !kv->page_table || !index || !index_count ||
@@ -1115,6 +1134,8 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   prm.cap = index_capacity;
   prm.out = out;
   prm.lse = lse;
+  prm.logits = logits;
+  if (logits && seq_len) return ZOOMR_ERR_INVALID_ARG;
   const size_t part = attn_ws_part_floats(geom, batch) * sizeof(float);
   prm.ws_part = (float *)workspace;
   prm.ws_cnt = (int32_t *)((char *)workspace + ((part + 255) / 256) * 256);
@@ -1146,7 +1167,7 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   }
 #define ZOOMR_AT(DD, GG)                                                                 \
   do {                                                                                   \
-    auto kfn = sparse_attn_kernel<DD, GG>;                                               \
+    auto kfn = logits ? sparse_attn_kernel<DD, GG, true> : sparse_attn_kernel<DD, GG>;   \
     const size_t smem = attn_smem_bytes<DD, GG>(batch);                                  \
     if (smem > 227 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                 \
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
@@ -1190,6 +1211,16 @@ extern "C" int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batc
   if (!lse) return ZOOMR_ERR_INVALID_ARG;
   return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, nullptr, 0, 0,
                             softmax_scale, out, lse, workspace, workspace_bytes, dev_status, stream);
+}
+
+extern "C" int zoomr_sparse_decode_attn_logits(const zoomr_geom *geom, int32_t batch, const void *q,
+                                               const zoomr_kv *kv, const int32_t *index, const int32_t *index_count,
+                                               int32_t index_capacity, float softmax_scale, float *out, float *lse,
+                                               float *logits, void *workspace, size_t workspace_bytes,
+                                               int32_t *dev_status, void *stream) {
+  if (!lse || !logits) return ZOOMR_ERR_INVALID_ARG;
+  return sparse_decode_attn(geom, batch, q, kv, index, nullptr, index_count, index_capacity, nullptr, 0, 0,
+                            softmax_scale, out, lse, workspace, workspace_bytes, dev_status, stream, logits);
 }
 
 extern "C" const char *zoomr_status_str(int status) {

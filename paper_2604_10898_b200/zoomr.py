@@ -24,7 +24,8 @@ A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
 EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
            "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
            "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
-           "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_status_str", "zoomr_abi_version")
+           "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
+           "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -48,7 +49,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 4  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 5  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -85,6 +86,13 @@ def lib():
         L.zoomr_sparse_decode_attn_lse.restype = C.c_int
         L.zoomr_merge_attn.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_merge_attn.restype = C.c_int
+        L.zoomr_sparse_decode_attn_logits.argtypes = [vp, i32, vp, vp, vp, vp, i32, C.c_float, vp, vp, vp, vp, sz,
+                                                      vp, vp]
+        L.zoomr_sparse_decode_attn_logits.restype = C.c_int
+        L.zoomr_h2o_accumulate.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp]
+        L.zoomr_h2o_accumulate.restype = C.c_int
+        L.zoomr_h2o_select.argtypes = [i32, vp, vp, i32, vp, i32, vp, i32, i32, i32, vp, vp, vp, vp]
+        L.zoomr_h2o_select.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -268,6 +276,52 @@ def merge_attn(shape: Shape, part_out, part_lse, out, part_count=None, lse=None,
                                 _ptr(part_count, torch.int32, "part_count"), _ptr(out, torch.float32, "out"),
                                 _ptr(lse, torch.float32, "lse"), _stream(stream))
     _check("zoomr_merge_attn", rc)
+
+
+def sparse_decode_attn_logits(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out, lse, logits,
+                              workspace, softmax_scale=None, dev_status=None, stream=None):
+    """a5 writing also lse [B][L][H_q] and logits [B][L][H_q][cap] (zoomr_sparse_decode_attn_logits)."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
+    if logits.shape[-1] != index.shape[1]:
+        raise ValueError("logits' last dimension must be the index capacity")
+    rc = lib().zoomr_sparse_decode_attn_logits(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv),
+                                               _ptr(index, torch.int32, "index"),
+                                               _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                               C.c_float(sc), _ptr(out, torch.float32, "out"),
+                                               _ptr(lse, torch.float32, "lse"), _ptr(logits, torch.float32, "logits"),
+                                               _ptr(workspace, None, "workspace"),
+                                               workspace.numel() * workspace.element_size(),
+                                               _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_sparse_decode_attn_logits", rc)
+
+
+def h2o_accumulate(shape: Shape, index, index_count, logits, lse, score, index_copy=None, count_copy=None,
+                   dev_status=None, stream=None):
+    """score[b, index[b,i]] += mean_{l,h} exp(logits - lse) (zoomr_h2o_accumulate). score fp32 [B][stride]."""
+    g = shape.c()
+    rc = lib().zoomr_h2o_accumulate(C.byref(g), index.shape[0], _ptr(index, torch.int32, "index"),
+                                    _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                    _ptr(logits, torch.float32, "logits"), _ptr(lse, torch.float32, "lse"),
+                                    _ptr(score, torch.float32, "score"), score.shape[1],
+                                    _ptr(index_copy, torch.int32, "index_copy"),
+                                    _ptr(count_copy, torch.int32, "count_copy"),
+                                    _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_h2o_accumulate", rc)
+
+
+def h2o_select(prev_index, prev_count, score, seq_len, sink, window, budget, index, index_count, dev_status=None,
+               stream=None):
+    """The next H2O retained set (zoomr_h2o_select)."""
+    if prev_index.shape != index.shape:
+        raise ValueError("prev_index and index must have the same shape")
+    rc = lib().zoomr_h2o_select(index.shape[0], _ptr(prev_index, torch.int32, "prev_index"),
+                                _ptr(prev_count, torch.int32, "prev_count"), index.shape[1],
+                                _ptr(score, torch.float32, "score"), score.shape[1],
+                                _ptr(seq_len, torch.int32, "seq_len"), int(sink), int(window), int(budget),
+                                _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),
+                                _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_h2o_select", rc)
 
 
 def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:

@@ -18,7 +18,8 @@
  * plus the fused select (a1..a4 in one launch), Algorithm 1's per-token
  * bookkeeping (KV append, segment tracking), the token-sharded split-K
  * pieces (index restriction, a5 with log-sum-exp, the merge) and the H2O
- * comparison policy (a5 with logits, score accumulation, eviction).
+ * comparison policy (a5 with logits, score accumulation, eviction) and the
+ * host-memory tier (HBM hot pool caching a pinned host cache).
  *
  * Conventions shared by every call
  *  - Ownership: every array argument is DEVICE memory allocated and owned by
@@ -50,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 5
+#define ZOOMR_ABI_VERSION 6
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -276,7 +277,9 @@ int zoomr_shard_index(int32_t batch, const int32_t *index, const int32_t *index_
  * exp(q[b,l,h] . k_j * softmax_scale).  Arguments as zoomr_sparse_decode_attn
  * without the phase-A rows (seq_len = NULL); lse must be non-NULL.  A sequence
  * with index_count 0 is skipped: its out and lse rows are left untouched (the
- * merge below excludes it through part_count). */
+ * merge below excludes it through part_count).  Nothing is read before the
+ * preceding kernel on the stream has completed -- the page table included, so
+ * it may be that kernel's output (zoomr_tier_fetch's residency table). */
 int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
                                  const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                  const int32_t *index_count, int32_t index_capacity, float softmax_scale,
@@ -338,6 +341,31 @@ int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *pr
                      int32_t index_capacity, const float *score, int32_t score_stride,
                      const int32_t *seq_len, int32_t sink, int32_t window, int32_t budget, int32_t *index,
                      int32_t *index_count, int32_t *dev_status, void *stream);
+
+/* ---- Host-memory tier (the paper's system) -------------
+ * The full cache lives in pinned host memory (host_kv: same layout and page
+ * table as zoomr_kv; k and v must be device-accessible, i.e. pinned with
+ * cudaHostAlloc / cudaHostRegister, read through their unified addresses).
+ * HBM holds a hot pool of hot_pages pages (hot_k, hot_v: bf16
+ * [L][hot_pages][H_kv][P][d]) caching it, with
+ *   hot_page_table int32 [B][max_pages]: logical page -> hot page or -1,
+ *   hot_owner      int32 [hot_pages]: b*max_pages + logical page, or -1 (free),
+ *   hot_stamp      int32 [hot_pages]: last step the page was used, -1 if never;
+ * initialised by the caller to -1 / -1 / -1; workspace zero-filled once.
+ * zoomr_tier_fetch makes every page that I_f (index / index_count, as a4
+ * writes it) touches resident: pages already resident are stamped with the
+ * step; each missing page takes, in page order, the least recently used hot
+ * page (smallest (stamp, page)) among those this step does not touch, and is
+ * copied from the host (all layers, K and V).  Afterwards a5 runs on the hot
+ * pool (zoomr_kv {hot_k, hot_v, hot_pages, hot_page_table, max_pages}) through
+ * zoomr_sparse_decode_attn_lse, which reads nothing before this call's kernels
+ * have completed.  Device errors: CAPACITY (the hot pool cannot hold the
+ * pages of this step's I_f; the rest stay missing), INDEX_RANGE. */
+size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t max_pages, int32_t hot_pages);
+int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k, void *hot_v,
+                     int32_t hot_pages, int32_t *hot_page_table, int32_t *hot_owner, int32_t *hot_stamp,
+                     const int32_t *index, const int32_t *index_count, int32_t index_capacity,
+                     void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

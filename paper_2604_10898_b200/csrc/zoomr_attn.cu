@@ -1143,7 +1143,10 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   prm.L = geom->num_layers;
   prm.Hkv = geom->num_kv_heads;
   prm.P = geom->page_size;
-  prm.pt_smem = (int64_t)batch * kv->max_pages <= kPtSmem;
+  // the page table is staged in shared memory before the wait, except in the
+  // lse / logits variants, where it may be the preceding kernel's output (the
+  // host tier's residency table): read from global memory after the wait
+  prm.pt_smem = !lse && (int64_t)batch * kv->max_pages <= kPtSmem;
   prm.Pshift = -1;
   for (int sft = 0; sft < 31; ++sft)
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;

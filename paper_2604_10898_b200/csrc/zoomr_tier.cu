@@ -1,0 +1,258 @@
+// Host-memory tier (the paper's own system, P:103-109:
+// "we offload these initial KVs to CPU memory ... only the subset of the KV
+// cache specified by the index set" is loaded per step).
+//
+// B200 design: the full cache lives in pinned host memory (mapped, so kernels
+// read it over PCIe / C2C through its unified address); HBM holds a HOT POOL
+// of pages that caches it.  Per step, after I_f is known:
+//   zoomr_tier_fetch = plan (one CTA: which logical pages I_f touches, which
+//   of them are not resident, least-recently-used victims among the pages
+//   this step does not touch) + copy (all SMs: the missing pages, every layer,
+//   K and V, host -> hot pool), then a5 runs on the hot pool.
+// Because I_f changes little from step to step (the window advances one token,
+// zoomed segments change at semantic boundaries), the steady-state transfer is
+// the pages that ENTERED I_f, not I_f itself (the paper reloads I_f per layer).
+#include "common.cuh"
+
+namespace zoomr {
+
+constexpr int kPlanThreads = 1024;
+
+__device__ __forceinline__ int tier_block_scan(int x, int *wsum, int *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = wsum[lane];
+    int vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) vi += y;
+    }
+    wsum[lane] = vi - v;
+    if (lane == 31) wsum[32] = vi;
+  }
+  __syncthreads();
+  const int r = wsum[warp] + incl - x;
+  *total = wsum[32];
+  __syncthreads();
+  return r;
+}
+
+// ws layout (int32): [0] step counter, [1] n_fetch, then need[B*max_pages] (as int32),
+// missing[hot_pages], fetch_hot[hot_pages], fetch_host[hot_pages]
+__global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
+    int32_t B, const int32_t *__restrict__ index, const int32_t *__restrict__ count, int32_t cap, int32_t P,
+    int32_t max_pages, const int32_t *__restrict__ host_pt, int32_t *__restrict__ hot_pt,
+    int32_t *__restrict__ owner, int32_t *__restrict__ stamp, int32_t hot_pages, int32_t *__restrict__ ws,
+    int32_t *status) {
+  __shared__ int wsum[33];
+  __shared__ int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_need;
+  const int tid = threadIdx.x;
+  const int NP = B * max_pages;
+  int32_t *need = ws + 2, *missing = need + NP, *fetch_hot = missing + hot_pages, *fetch_host = fetch_hot + hot_pages;
+  const int step = ws[0] + 1;
+  // 1. pages touched by I_f
+  for (int x = tid; x < NP; x += kPlanThreads) need[x] = 0;
+  __syncthreads();
+  for (int b = 0; b < B; ++b) {
+    int n = count[b];
+    n = n < cap ? n : cap;
+    for (int i = tid; i < n; i += kPlanThreads) {
+      const int t = index[(int64_t)b * cap + i];
+      const int lp = t / P;
+      if (t < 0 || lp >= max_pages) set_status(status, ZOOMR_ERR_INDEX_RANGE);
+      else need[b * max_pages + lp] = 1;
+    }
+  }
+  __syncthreads();
+  // 2. resident ones are stamped with this step; the others are missing (in page order)
+  int nmiss = 0;
+  for (int x0 = 0; x0 < NP; x0 += kPlanThreads) {
+    const int x = x0 + tid;
+    bool miss = false;
+    if (x < NP && need[x]) {
+      const int h = hot_pt[x];
+      if (h >= 0 && h < hot_pages) stamp[h] = step;
+      else miss = true;
+    }
+    int tot;
+    const int off = tier_block_scan(miss ? 1 : 0, wsum, &tot);
+    if (miss && nmiss + off < hot_pages) missing[nmiss + off] = x;
+    nmiss += tot;
+  }
+  __syncthreads();  // the stamps above are visible to the victim search
+  // 3. victims: the nmiss least recently used hot pages this step does not touch
+  //    (free pages have stamp -1); key (stamp + 1, page) -- unique
+  int ncand = 0;
+  for (int h0 = 0; h0 < hot_pages; h0 += kPlanThreads) {
+    const int h = h0 + tid;
+    int tot;
+    tier_block_scan((h < hot_pages && stamp[h] < step) ? 1 : 0, wsum, &tot);
+    ncand += tot;
+  }
+  if (nmiss > ncand) {  // the hot pool cannot hold this step's I_f
+    if (tid == 0) set_status(status, ZOOMR_ERR_CAPACITY);
+    nmiss = ncand;
+  }
+  unsigned long long thr = ~0ull;  // victims: candidate keys <= thr
+  if (nmiss > 0 && nmiss < ncand) {  // radix select of the nmiss-th smallest key, MSB first
+    if (tid == 0) {
+      s_prefix = 0ull;
+      s_need = nmiss;
+    }
+    unsigned long long mask = 0ull;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int shift = 56 - 8 * pass;
+      if (tid < 256) hist[tid] = 0;
+      __syncthreads();
+      const unsigned long long prefix = s_prefix;
+      for (int h = tid; h < hot_pages; h += kPlanThreads) {
+        if (stamp[h] >= step) continue;
+        const unsigned long long k = ((unsigned long long)(uint32_t)(stamp[h] + 1) << 32) | (uint32_t)h;
+        if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (tid < 32) {  // digit d with below(d) < need <= below(d) + hist[d] (ascending)
+        const int lane = tid;
+        int hh[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          hh[j] = hist[8 * lane + j];
+          sum += hh[j];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int need_ = s_need;
+        int below = incl - sum, found = -1, nbelow = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (found < 0 && below < need_ && need_ <= below + hh[j]) {
+            found = 8 * lane + j;
+            nbelow = below;
+          }
+          below += hh[j];
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+        const int src = __ffs(bal) - 1;
+        found = __shfl_sync(0xffffffffu, found, src);
+        nbelow = __shfl_sync(0xffffffffu, nbelow, src);
+        if (lane == 0) {
+          s_prefix = prefix | ((unsigned long long)found << shift);
+          s_need = need_ - nbelow;
+        }
+      }
+      mask |= 0xffull << shift;
+      __syncthreads();
+    }
+    thr = s_prefix;
+  }
+  // 4. victims in page order take the missing pages in page order
+  int nv = 0;
+  for (int h0 = 0; h0 < hot_pages && nmiss > 0; h0 += kPlanThreads) {
+    const int h = h0 + tid;
+    bool v = false;
+    if (h < hot_pages && stamp[h] < step) {
+      const unsigned long long k = ((unsigned long long)(uint32_t)(stamp[h] + 1) << 32) | (uint32_t)h;
+      v = k <= thr;
+    }
+    int tot;
+    const int j = nv + tier_block_scan(v ? 1 : 0, wsum, &tot);
+    if (v && j < nmiss) {
+      const int x = missing[j];
+      const int old = owner[h];
+      if (old >= 0 && old < NP) hot_pt[old] = -1;  // evicted (not needed this step)
+      owner[h] = x;
+      hot_pt[x] = h;
+      stamp[h] = step;
+      const int hp = host_pt[x];
+      fetch_hot[j] = h;
+      fetch_host[j] = hp;
+      if (hp < 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
+    }
+    nv += tot;
+  }
+  if (tid == 0) {
+    ws[0] = step;
+    ws[1] = nmiss;
+  }
+}
+
+// all SMs: work item w = (fetch j, layer l, K or V) copies the contiguous
+// H_kv*P*d block of host page fetch_host[j] to hot page fetch_hot[j]
+__global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict__ host_k,
+                                                         const uint4 *__restrict__ host_v, int64_t host_pages,
+                                                         uint4 *__restrict__ hot_k, uint4 *__restrict__ hot_v,
+                                                         int64_t hot_pages, int32_t L, int32_t blk16,
+                                                         const int32_t *__restrict__ ws, int32_t NP) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int nf = ws[1];
+  const int32_t *fetch_hot = ws + 2 + NP + hot_pages, *fetch_host = fetch_hot + hot_pages;
+  const int64_t items = (int64_t)nf * L * 2;
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int kv = (int)(w & 1);
+    const int64_t jl = w >> 1;
+    const int j = (int)(jl / L), l = (int)(jl - (int64_t)j * L);
+    const int hp = fetch_host[j], hh = fetch_hot[j];
+    if (hp < 0 || hp >= host_pages) continue;
+    const uint4 *src = (kv ? host_v : host_k) + ((int64_t)l * host_pages + hp) * blk16;
+    uint4 *dst = (kv ? hot_v : hot_k) + ((int64_t)l * hot_pages + hh) * blk16;
+    int e = threadIdx.x;
+    for (; e + 3 * 256 < blk16; e += 4 * 256) {  // four 16-byte host reads in flight per thread
+      const uint4 a = __ldcs(src + e), b = __ldcs(src + e + 256), c = __ldcs(src + e + 512), d = __ldcs(src + e + 768);
+      dst[e] = a;
+      dst[e + 256] = b;
+      dst[e + 512] = c;
+      dst[e + 768] = d;
+    }
+    for (; e < blk16; e += 256) dst[e] = __ldcs(src + e);
+  }
+}
+
+}  // namespace zoomr
+
+using namespace zoomr;
+
+extern "C" size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t max_pages, int32_t hot_pages) {
+  if (batch < 1 || max_pages < 1 || hot_pages < 1) return 0;
+  return sizeof(int32_t) * (2 + (size_t)batch * max_pages + 3 * (size_t)hot_pages);
+}
+
+extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k,
+                                void *hot_v, int32_t hot_pages, int32_t *hot_page_table, int32_t *hot_owner,
+                                int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
+                                int32_t index_capacity, void *workspace, size_t workspace_bytes,
+                                int32_t *dev_status, void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !host_kv || !host_kv->k || !host_kv->v || !host_kv->page_table || host_kv->num_pages < 1 ||
+      host_kv->max_pages < 1 || !hot_k || !hot_v || hot_pages < 1 || !hot_page_table || !hot_owner || !hot_stamp ||
+      !index || !index_count || index_capacity < 1 || !workspace)
+    return ZOOMR_ERR_INVALID_ARG;
+  if (workspace_bytes < zoomr_tier_workspace_bytes(batch, host_kv->max_pages, hot_pages)) return ZOOMR_ERR_WORKSPACE;
+  const int64_t blk = (int64_t)geom->num_kv_heads * geom->page_size * geom->head_dim * 2;  // bytes per (page, layer)
+  if (blk % 16) return ZOOMR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  tier_plan_kernel<<<1, kPlanThreads, 0, s>>>(batch, index, index_count, index_capacity, geom->page_size,
+                                              host_kv->max_pages, host_kv->page_table, hot_page_table, hot_owner,
+                                              hot_stamp, hot_pages, (int32_t *)workspace, dev_status);
+  rc = launch_status();
+  if (rc) return rc;
+  launch_pdl(tier_copy_kernel, 2 * num_sms(), 256, 0, s, (const uint4 *)host_kv->k, (const uint4 *)host_kv->v,
+             (int64_t)host_kv->num_pages, (uint4 *)hot_k, (uint4 *)hot_v, (int64_t)hot_pages, geom->num_layers,
+             (int32_t)(blk / 16), (const int32_t *)workspace, batch * host_kv->max_pages);
+  return launch_status();
+}

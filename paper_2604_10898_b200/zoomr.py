@@ -25,7 +25,8 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
            "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
-           "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_status_str", "zoomr_abi_version")
+           "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
+           "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -49,7 +50,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 5  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 6  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -93,6 +94,10 @@ def lib():
         L.zoomr_h2o_accumulate.restype = C.c_int
         L.zoomr_h2o_select.argtypes = [i32, vp, vp, i32, vp, i32, vp, i32, i32, i32, vp, vp, vp, vp]
         L.zoomr_h2o_select.restype = C.c_int
+        L.zoomr_tier_workspace_bytes.argtypes = [i32, i32, i32]
+        L.zoomr_tier_workspace_bytes.restype = sz
+        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp]
+        L.zoomr_tier_fetch.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -322,6 +327,36 @@ def h2o_select(prev_index, prev_count, score, seq_len, sink, window, budget, ind
                                 _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),
                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_h2o_select", rc)
+
+
+def _host_ptr(t, name):
+    """A pinned host tensor's unified address (device-accessible); raises if not pinned."""
+    if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_pinned():
+        raise TypeError(f"{name} must be a pinned host tensor")
+    if t.dtype != torch.bfloat16 or not t.is_contiguous():
+        raise TypeError(f"{name} must be contiguous bf16")
+    return C.c_void_p(t.data_ptr())
+
+
+def tier_workspace_bytes(batch: int, max_pages: int, hot_pages: int) -> int:
+    return int(lib().zoomr_tier_workspace_bytes(int(batch), int(max_pages), int(hot_pages)))
+
+
+def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_table, hot_owner, hot_stamp,
+               index, index_count, workspace, dev_status=None, stream=None):
+    """Make the pages of I_f resident in the HBM hot pool (zoomr_tier_fetch). host_k/v: pinned bf16."""
+    g = shape.c()
+    kv = KV(_host_ptr(host_k, "host_k"), _host_ptr(host_v, "host_v"), host_k.shape[1],
+            _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
+    rc = lib().zoomr_tier_fetch(C.byref(g), index.shape[0], C.byref(kv), _ptr(hot_k, torch.bfloat16, "hot_k"),
+                                _ptr(hot_v, torch.bfloat16, "hot_v"), hot_k.shape[1],
+                                _ptr(hot_page_table, torch.int32, "hot_page_table"),
+                                _ptr(hot_owner, torch.int32, "hot_owner"), _ptr(hot_stamp, torch.int32, "hot_stamp"),
+                                _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),
+                                index.shape[1], _ptr(workspace, None, "workspace"),
+                                workspace.numel() * workspace.element_size(),
+                                _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_tier_fetch", rc)
 
 
 def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:

@@ -308,6 +308,81 @@ def token_shard_section(shape, prm, s0, cfg, K, world_sim=8):
                     "shard_index + a5 with lse over its part of I_f; NVLink all-gather not included"}
 
 
+def host_tier_section(shape, prm, s0, cfg, K, hot_frac=0.7):
+    """NEXT-2: the cache in pinned host memory, an HBM hot pool of hot_frac of its pages."""
+    from paper_2604_10898_b200.tier import HostTierStep
+    inp = s0["inp"]
+    pages_total = int(inp.k_pool.shape[1])
+    hot_pages = int(hot_frac * pages_total)
+    B = inp.q.shape[0]
+    host_k, host_v = inp.k_pool.cpu().pin_memory(), inp.v_pool.cpu().pin_memory()
+    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, hot_pages)
+    st.mean_keys.copy_(s0["st"].mean_keys)
+    seg = s0["seg"]
+    page_bytes = 2 * cfg.L * cfg.Hkv * cfg.page * cfg.d * 2  # K and V, every layer
+
+    def ev_time(fn, n=1):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / n  # us
+
+    def reset():
+        st.hot_page_table.fill_(-1)
+        st.hot_owner.fill_(-1)
+        st.hot_stamp.fill_(-1)
+    qa = inp.q
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qb = (torch.randn(qa.shape, device="cuda", generator=g)).bfloat16()  # another query: other zoomed segments
+    st.run(qa, seg)
+    cold = []
+    for _ in range(3):
+        reset()
+        cold.append(ev_time(lambda: st.run(qa, seg)))
+        st.check_status()
+    n_cold = st.fetched_pages()
+    warm = ev_time(lambda: st.run(qa, seg), K)
+    # churn: alternate two queries (other zoomed segments) with a hot pool only 8 pages larger
+    # than one step's pages, so each switch evicts and refetches
+    tight = n_cold + 8
+    del st
+    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, tight)
+    st.mean_keys.copy_(s0["st"].mean_keys)
+    st.run(qa, seg)
+    st.run(qb, seg)
+    torch.cuda.synchronize()
+    n_switch = []
+
+    def alt(i=[0]):
+        st.run(qa if i[0] % 2 == 0 else qb, seg)
+        i[0] += 1
+    churn = ev_time(alt, 20)
+    for q_ in (qa, qb):
+        st.run(q_, seg)
+        torch.cuda.synchronize()
+        n_switch.append(st.fetched_pages())
+    st.check_status()
+    # the host link: one pinned 256 MB host -> device copy
+    hb = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    db = torch.empty_like(hb, device="cuda")
+    link = hb.numel() / (ev_time(lambda: db.copy_(hb, non_blocking=True), 5) * 1e-6) / 1e9
+    cold_us = sorted(cold)[1]
+    return {"pages_total": pages_total, "hot_pages": hot_pages, "hot_pool_bytes": hot_pages * page_bytes,
+            "host_cache_bytes": host_k.numel() * 4,
+            "cold_step_us": cold_us, "cold_pages_fetched": n_cold, "cold_bytes": n_cold * page_bytes,
+            "cold_fetch_gbs": n_cold * page_bytes / ((cold_us - warm) * 1e-6) / 1e9,
+            "warm_step_us": warm, "alternating_hot_pages": tight, "alternating_queries_us_per_step": churn,
+            "alternating_pages_per_switch": n_switch, "host_link_memcpy_gbs": link,
+            "note": "cache in pinned host memory, hot pool = 70% of its pages; per step: fused select + tier "
+                    "fetch (plan + copy of the missing pages over the host link) + a5 on the hot pool; "
+                    "alternating: two queries with different zoomed segments, one after the other, hot pool = "
+                    "one step's pages + 8"}
+
+
 def run_ours(args):
     rank, world, local = init_dist(args.gpus)
     import zoomr_synth as S
@@ -480,6 +555,9 @@ def run_ours(args):
     token_sharded = None
     if world == 1 and not args.no_loop:
         token_sharded = token_shard_section(shape, prm, sets[0], cfg, K)
+    host_tier = None
+    if world == 1 and not args.no_loop:
+        host_tier = host_tier_section(shape, prm, sets[0], cfg, K)
     # per-stage breakdown (informational): each stage alone, graph-replayed
     stages = {}
     s0 = sets[0]
@@ -548,6 +626,7 @@ def run_ours(args):
         "decode_loop": decode_loop,
         "policies": policies,
         "token_sharded": token_sharded,
+        "host_tier": host_tier,
         "e2e": {"value": world * Bseq * K / t_e2e, "unit": "seqs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": sum(full_launch if is_full(i) else light_launch for i in range(K)),

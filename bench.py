@@ -308,18 +308,14 @@ def token_shard_section(shape, prm, s0, cfg, K, world_sim=8):
                     "shard_index + a5 with lse over its part of I_f; NVLink all-gather not included"}
 
 
-def host_tier_section(shape, prm, s0, cfg, K, hot_frac=0.7):
-    """NEXT-2: the cache in pinned host memory, an HBM hot pool of hot_frac of its pages."""
+def host_tier_section(shape, prm, s0, cfg, K, hot_page_sizes=(64, 16)):
+    """NEXT-2: the cache in pinned host memory, an HBM hot pool caching its pages."""
     from paper_2604_10898_b200.tier import HostTierStep
     inp = s0["inp"]
-    pages_total = int(inp.k_pool.shape[1])
-    hot_pages = int(hot_frac * pages_total)
     B = inp.q.shape[0]
     host_k, host_v = inp.k_pool.cpu().pin_memory(), inp.v_pool.cpu().pin_memory()
-    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, hot_pages)
-    st.mean_keys.copy_(s0["st"].mean_keys)
     seg = s0["seg"]
-    page_bytes = 2 * cfg.L * cfg.Hkv * cfg.page * cfg.d * 2  # K and V, every layer
+    cache_bytes = host_k.numel() * 4  # K and V
 
     def ev_time(fn, n=1):
         torch.cuda.synchronize()
@@ -331,56 +327,65 @@ def host_tier_section(shape, prm, s0, cfg, K, hot_frac=0.7):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e3 / n  # us
 
-    def reset():
-        st.hot_page_table.fill_(-1)
-        st.hot_owner.fill_(-1)
-        st.hot_stamp.fill_(-1)
+    def make(ph, hot_pages):
+        st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, hot_pages,
+                          hot_page_size=ph)
+        st.mean_keys.copy_(s0["st"].mean_keys)
+        return st
     qa = inp.q
     g = torch.Generator(device="cuda").manual_seed(5)
     qb = (torch.randn(qa.shape, device="cuda", generator=g)).bfloat16()  # another query: other zoomed segments
-    st.run(qa, seg)
-    cold = []
-    for _ in range(3):
-        reset()
-        cold.append(ev_time(lambda: st.run(qa, seg)))
-        st.check_status()
-    n_cold = st.fetched_pages()
-    warm = ev_time(lambda: st.run(qa, seg), K)
-    # churn: alternate two queries (other zoomed segments) with a hot pool only 8 pages larger
-    # than one step's pages, so each switch evicts and refetches
-    tight = n_cold + 8
-    del st
-    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, tight)
-    st.mean_keys.copy_(s0["st"].mean_keys)
-    st.run(qa, seg)
-    st.run(qb, seg)
-    torch.cuda.synchronize()
-    n_switch = []
-
-    def alt(i=[0]):
-        st.run(qa if i[0] % 2 == 0 else qb, seg)
-        i[0] += 1
-    churn = ev_time(alt, 20)
-    for q_ in (qa, qb):
-        st.run(q_, seg)
+    res = {}
+    for ph in hot_page_sizes:
+        if cfg.page % ph:
+            continue
+        page_bytes = 2 * cfg.L * cfg.Hkv * ph * cfg.d * 2  # K and V, every layer
+        all_pages = int(inp.k_pool.shape[1]) * (cfg.page // ph)
+        st = make(ph, all_pages)
+        cold = []
+        for _ in range(3):
+            st.hot_page_table.fill_(-1)
+            st.hot_owner.fill_(-1)
+            st.hot_stamp.fill_(-1)
+            cold.append(ev_time(lambda: st.run(qa, seg)))
+            st.check_status()
+        n_cold = st.fetched_pages()
+        warm = ev_time(lambda: st.run(qa, seg), K)
+        cold_us = sorted(cold)[1]
+        # churn: the two queries alternate on a pool 8 pages larger than one step's pages
+        del st
+        tight = n_cold + 8
+        st = make(ph, tight)
+        st.run(qa, seg)
+        st.run(qb, seg)
         torch.cuda.synchronize()
-        n_switch.append(st.fetched_pages())
-    st.check_status()
-    # the host link: one pinned 256 MB host -> device copy
+        i = [0]
+
+        def alt():
+            st.run(qa if i[0] % 2 == 0 else qb, seg)
+            i[0] += 1
+        churn = ev_time(alt, 20)
+        sw = []
+        for q_ in (qa, qb):
+            st.run(q_, seg)
+            torch.cuda.synchronize()
+            sw.append(st.fetched_pages())
+        st.check_status()
+        del st
+        res[f"hot_page_{ph}"] = {
+            "cold_pages": n_cold, "cold_bytes": n_cold * page_bytes, "hbm_saving": cache_bytes / (n_cold * page_bytes),
+            "cold_step_us": cold_us, "cold_fetch_gbs": n_cold * page_bytes / ((cold_us - warm) * 1e-6) / 1e9,
+            "warm_step_us": warm, "alternating_pool_pages": tight, "alternating_us_per_step": churn,
+            "alternating_pages_per_switch": sw}
     hb = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     db = torch.empty_like(hb, device="cuda")
-    link = hb.numel() / (ev_time(lambda: db.copy_(hb, non_blocking=True), 5) * 1e-6) / 1e9
-    cold_us = sorted(cold)[1]
-    return {"pages_total": pages_total, "hot_pages": hot_pages, "hot_pool_bytes": hot_pages * page_bytes,
-            "host_cache_bytes": host_k.numel() * 4,
-            "cold_step_us": cold_us, "cold_pages_fetched": n_cold, "cold_bytes": n_cold * page_bytes,
-            "cold_fetch_gbs": n_cold * page_bytes / ((cold_us - warm) * 1e-6) / 1e9,
-            "warm_step_us": warm, "alternating_hot_pages": tight, "alternating_queries_us_per_step": churn,
-            "alternating_pages_per_switch": n_switch, "host_link_memcpy_gbs": link,
-            "note": "cache in pinned host memory, hot pool = 70% of its pages; per step: fused select + tier "
-                    "fetch (plan + copy of the missing pages over the host link) + a5 on the hot pool; "
-                    "alternating: two queries with different zoomed segments, one after the other, hot pool = "
-                    "one step's pages + 8"}
+    res["host_link_memcpy_gbs"] = hb.numel() / (ev_time(lambda: db.copy_(hb, non_blocking=True), 5) * 1e-6) / 1e9
+    res["host_cache_bytes"] = cache_bytes
+    res["note"] = ("cache in pinned host memory; per step: fused select + tier fetch (plan + copy of the missing "
+                   "hot pages over the host link) + a5 on the HBM hot pool; hbm_saving = cache bytes / hot bytes "
+                   "one step needs; alternating: two queries with different zoomed segments on a pool of one "
+                   "step's pages + 8")
+    return res
 
 
 def run_ours(args):

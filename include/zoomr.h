@@ -346,26 +346,31 @@ int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *pr
  * The full cache lives in pinned host memory (host_kv: same layout and page
  * table as zoomr_kv; k and v must be device-accessible, i.e. pinned with
  * cudaHostAlloc / cudaHostRegister, read through their unified addresses).
- * HBM holds a hot pool of hot_pages pages (hot_k, hot_v: bf16
- * [L][hot_pages][H_kv][P][d]) caching it, with
- *   hot_page_table int32 [B][max_pages]: logical page -> hot page or -1,
- *   hot_owner      int32 [hot_pages]: b*max_pages + logical page, or -1 (free),
+ * HBM holds a hot pool of hot_pages pages of hot_page_size tokens (Ph, a
+ * divisor of the host page size P; R = P / Ph) caching it:
+ *   hot_k, hot_v   bf16 [L][hot_pages][H_kv][Ph][d],
+ *   hot_page_table int32 [B][max_pages * R]: hot logical page (tokens
+ *                  [j*Ph, (j+1)*Ph) of sequence b) -> hot page or -1,
+ *   hot_owner      int32 [hot_pages]: b*max_pages*R + hot logical page, or -1 (free),
  *   hot_stamp      int32 [hot_pages]: last step the page was used, -1 if never;
- * initialised by the caller to -1 / -1 / -1; workspace zero-filled once.
- * zoomr_tier_fetch makes every page that I_f (index / index_count, as a4
- * writes it) touches resident: pages already resident are stamped with the
- * step; each missing page takes, in page order, the least recently used hot
- * page (smallest (stamp, page)) among those this step does not touch, and is
- * copied from the host (all layers, K and V).  Afterwards a5 runs on the hot
- * pool (zoomr_kv {hot_k, hot_v, hot_pages, hot_page_table, max_pages}) through
- * zoomr_sparse_decode_attn_lse, which reads nothing before this call's kernels
- * have completed.  Device errors: CAPACITY (the hot pool cannot hold the
- * pages of this step's I_f; the rest stay missing), INDEX_RANGE. */
-size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t max_pages, int32_t hot_pages);
+ * initialised by the caller to -1 / -1 / -1; workspace zero-filled once
+ * (zoomr_tier_workspace_bytes(batch, max_pages * R, hot_pages)).
+ * zoomr_tier_fetch makes every hot logical page that I_f (index / index_count,
+ * as a4 writes it) touches resident: pages already resident are stamped with
+ * the step; each missing page takes, in page order, the least recently used
+ * hot page (smallest (stamp, page)) among those this step does not touch, and
+ * its rows are copied from the host (all layers, K and V).  Afterwards a5 runs
+ * on the hot pool (geometry page_size = Ph, zoomr_kv {hot_k, hot_v, hot_pages,
+ * hot_page_table, max_pages * R}) through zoomr_sparse_decode_attn_lse, which
+ * reads nothing before this call's kernels have completed.  Device errors:
+ * CAPACITY (the hot pool cannot hold the pages of this step's I_f; the rest
+ * stay missing), INDEX_RANGE. */
+size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t hot_pages);
 int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k, void *hot_v,
-                     int32_t hot_pages, int32_t *hot_page_table, int32_t *hot_owner, int32_t *hot_stamp,
-                     const int32_t *index, const int32_t *index_count, int32_t index_capacity,
-                     void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
+                     int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table, int32_t *hot_owner,
+                     int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
+                     int32_t index_capacity, void *workspace, size_t workspace_bytes, int32_t *dev_status,
+                     void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

@@ -46,11 +46,14 @@ __device__ __forceinline__ int tier_block_scan(int x, int *wsum, int *total) {
   return r;
 }
 
-// ws layout (int32): [0] step counter, [1] n_fetch, then need[B*max_pages] (as int32),
-// missing[hot_pages], fetch_hot[hot_pages], fetch_host[hot_pages]
+// Hot pages may be smaller than host pages: Ph = P / R tokens.  Hot logical page
+// x = b*hmp + lph (hmp = max_pages * R) holds tokens [lph*Ph, (lph+1)*Ph) of
+// sequence b: sub-page lph % R of host page host_pt[b][lph / R].
+// ws layout (int32): [0] step counter, [1] n_fetch, then need[B*hmp] (as int32),
+// missing[hot_pages], fetch_hot[hot_pages], fetch_host[hot_pages] (= host page * R + sub-page)
 __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
-    int32_t B, const int32_t *__restrict__ index, const int32_t *__restrict__ count, int32_t cap, int32_t P,
-    int32_t max_pages, const int32_t *__restrict__ host_pt, int32_t *__restrict__ hot_pt,
+    int32_t B, const int32_t *__restrict__ index, const int32_t *__restrict__ count, int32_t cap, int32_t Ph,
+    int32_t R, int32_t max_pages, const int32_t *__restrict__ host_pt, int32_t *__restrict__ hot_pt,
     int32_t *__restrict__ owner, int32_t *__restrict__ stamp, int32_t hot_pages, int32_t *__restrict__ ws,
     int32_t *status) {
   __shared__ int wsum[33];
@@ -58,7 +61,8 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
   __shared__ unsigned long long s_prefix;
   __shared__ int s_need;
   const int tid = threadIdx.x;
-  const int NP = B * max_pages;
+  const int hmp = max_pages * R;
+  const int NP = B * hmp;
   int32_t *need = ws + 2, *missing = need + NP, *fetch_hot = missing + hot_pages, *fetch_host = fetch_hot + hot_pages;
   const int step = ws[0] + 1;
   // 1. pages touched by I_f
@@ -69,9 +73,9 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
     n = n < cap ? n : cap;
     for (int i = tid; i < n; i += kPlanThreads) {
       const int t = index[(int64_t)b * cap + i];
-      const int lp = t / P;
-      if (t < 0 || lp >= max_pages) set_status(status, ZOOMR_ERR_INDEX_RANGE);
-      else need[b * max_pages + lp] = 1;
+      const int lp = t / Ph;
+      if (t < 0 || lp >= hmp) set_status(status, ZOOMR_ERR_INDEX_RANGE);
+      else need[b * hmp + lp] = 1;
     }
   }
   __syncthreads();
@@ -178,9 +182,10 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
       owner[h] = x;
       hot_pt[x] = h;
       stamp[h] = step;
-      const int hp = host_pt[x];
+      const int xb = x / hmp, lph = x - xb * hmp;
+      const int hp = host_pt[xb * max_pages + lph / R];
       fetch_hot[j] = h;
-      fetch_host[j] = hp;
+      fetch_host[j] = hp < 0 ? -1 : hp * R + lph % R;
       if (hp < 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
     }
     nv += tot;
@@ -191,13 +196,14 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
   }
 }
 
-// all SMs: work item w = (fetch j, layer l, K or V) copies the contiguous
-// H_kv*P*d block of host page fetch_host[j] to hot page fetch_hot[j]
+// all SMs: work item w = (fetch j, layer l, K or V) copies, for every KV head g,
+// the Ph*d block of sub-page (fetch_host[j] % R) of host page fetch_host[j] / R
+// to hot page fetch_hot[j]
 __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict__ host_k,
                                                          const uint4 *__restrict__ host_v, int64_t host_pages,
                                                          uint4 *__restrict__ hot_k, uint4 *__restrict__ hot_v,
-                                                         int64_t hot_pages, int32_t L, int32_t blk16,
-                                                         const int32_t *__restrict__ ws, int32_t NP) {
+                                                         int64_t hot_pages, int32_t L, int32_t Hkv, int32_t R,
+                                                         int32_t row16, const int32_t *__restrict__ ws, int32_t NP) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nf = ws[1];
   const int32_t *fetch_hot = ws + 2 + NP + hot_pages, *fetch_host = fetch_hot + hot_pages;
@@ -206,19 +212,28 @@ __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict_
     const int kv = (int)(w & 1);
     const int64_t jl = w >> 1;
     const int j = (int)(jl / L), l = (int)(jl - (int64_t)j * L);
-    const int hp = fetch_host[j], hh = fetch_hot[j];
+    const int hs = fetch_host[j], hh = fetch_hot[j];
+    const int hp = hs < 0 ? -1 : hs / R, sub = hs < 0 ? 0 : hs - hp * R;
     if (hp < 0 || hp >= host_pages) continue;
-    const uint4 *src = (kv ? host_v : host_k) + ((int64_t)l * host_pages + hp) * blk16;
-    uint4 *dst = (kv ? hot_v : hot_k) + ((int64_t)l * hot_pages + hh) * blk16;
+    // host block of (l, hp, g): R*row16 uint4; this sub-page: row16 of them at sub*row16
+    const uint4 *src = (kv ? host_v : host_k) + ((int64_t)l * host_pages + hp) * Hkv * R * row16 + sub * row16;
+    uint4 *dst = (kv ? hot_v : hot_k) + ((int64_t)l * hot_pages + hh) * Hkv * row16;
+    const int n16 = Hkv * row16;
     int e = threadIdx.x;
-    for (; e + 3 * 256 < blk16; e += 4 * 256) {  // four 16-byte host reads in flight per thread
-      const uint4 a = __ldcs(src + e), b = __ldcs(src + e + 256), c = __ldcs(src + e + 512), d = __ldcs(src + e + 768);
-      dst[e] = a;
-      dst[e + 256] = b;
-      dst[e + 512] = c;
-      dst[e + 768] = d;
+    for (; e + 3 * 256 < n16; e += 4 * 256) {  // four 16-byte host reads in flight per thread
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = e + u * 256, g = x / row16;
+        v[u] = __ldcs(src + (int64_t)g * R * row16 + (x - g * row16));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[e + u * 256] = v[u];
     }
-    for (; e < blk16; e += 256) dst[e] = __ldcs(src + e);
+    for (; e < n16; e += 256) {
+      const int g = e / row16;
+      dst[e] = __ldcs(src + (int64_t)g * R * row16 + (e - g * row16));
+    }
   }
 }
 
@@ -226,13 +241,14 @@ __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict_
 
 using namespace zoomr;
 
-extern "C" size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t max_pages, int32_t hot_pages) {
-  if (batch < 1 || max_pages < 1 || hot_pages < 1) return 0;
-  return sizeof(int32_t) * (2 + (size_t)batch * max_pages + 3 * (size_t)hot_pages);
+extern "C" size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t hot_pages) {
+  if (batch < 1 || hot_max_pages < 1 || hot_pages < 1) return 0;
+  return sizeof(int32_t) * (2 + (size_t)batch * hot_max_pages + 3 * (size_t)hot_pages);
 }
 
 extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k,
-                                void *hot_v, int32_t hot_pages, int32_t *hot_page_table, int32_t *hot_owner,
+                                void *hot_v, int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table,
+                                int32_t *hot_owner,
                                 int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
                                 int32_t index_capacity, void *workspace, size_t workspace_bytes,
                                 int32_t *dev_status, void *stream) {
@@ -242,17 +258,22 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
       host_kv->max_pages < 1 || !hot_k || !hot_v || hot_pages < 1 || !hot_page_table || !hot_owner || !hot_stamp ||
       !index || !index_count || index_capacity < 1 || !workspace)
     return ZOOMR_ERR_INVALID_ARG;
-  if (workspace_bytes < zoomr_tier_workspace_bytes(batch, host_kv->max_pages, hot_pages)) return ZOOMR_ERR_WORKSPACE;
-  const int64_t blk = (int64_t)geom->num_kv_heads * geom->page_size * geom->head_dim * 2;  // bytes per (page, layer)
-  if (blk % 16) return ZOOMR_ERR_UNSUPPORTED;
+  const int P = geom->page_size, Ph = hot_page_size;
+  if (Ph < 1 || P % Ph) return ZOOMR_ERR_INVALID_ARG;
+  const int R = P / Ph;
+  const int64_t hmp = (int64_t)host_kv->max_pages * R;
+  if (hmp * batch > 0x7fffffff || (int64_t)host_kv->num_pages * R > 0x7fffffff) return ZOOMR_ERR_UNSUPPORTED;
+  if (workspace_bytes < zoomr_tier_workspace_bytes(batch, (int32_t)hmp, hot_pages)) return ZOOMR_ERR_WORKSPACE;
+  const int64_t row = (int64_t)Ph * geom->head_dim * 2;  // bytes of one (page, layer, head) block of the hot pool
+  if (row % 16) return ZOOMR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
-  tier_plan_kernel<<<1, kPlanThreads, 0, s>>>(batch, index, index_count, index_capacity, geom->page_size,
-                                              host_kv->max_pages, host_kv->page_table, hot_page_table, hot_owner,
-                                              hot_stamp, hot_pages, (int32_t *)workspace, dev_status);
+  tier_plan_kernel<<<1, kPlanThreads, 0, s>>>(batch, index, index_count, index_capacity, Ph, R, host_kv->max_pages,
+                                              host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
+                                              (int32_t *)workspace, dev_status);
   rc = launch_status();
   if (rc) return rc;
   launch_pdl(tier_copy_kernel, 2 * num_sms(), 256, 0, s, (const uint4 *)host_kv->k, (const uint4 *)host_kv->v,
              (int64_t)host_kv->num_pages, (uint4 *)hot_k, (uint4 *)hot_v, (int64_t)hot_pages, geom->num_layers,
-             (int32_t)(blk / 16), (const int32_t *)workspace, batch * host_kv->max_pages);
+             geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp));
   return launch_status();
 }

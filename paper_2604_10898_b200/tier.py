@@ -19,20 +19,28 @@ from .step import StepParams, ZoomrStep
 class HostTierStep(ZoomrStep):
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int, params: StepParams,
                  host_k: torch.Tensor, host_v: torch.Tensor, page_table: torch.Tensor, hot_pages: int,
-                 device="cuda"):
-        super().__init__(shape, batch, max_summaries, index_capacity, params, device, early_known=False)
+                 device="cuda", hot_page_size: int = 0):
+        """shape: the host cache's geometry (page_size = P).  hot_page_size (default P) divides P:
+        smaller hot pages hold I_f with less HBM (a summary drags in Ph tokens, not P)."""
+        P = shape.page_size
+        Ph = hot_page_size or P
+        if P % Ph:
+            raise ValueError("hot_page_size must divide the host page size")
+        self.host_shape = shape
+        shape_hot = Z.Shape(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, Ph)
+        super().__init__(shape_hot, batch, max_summaries, index_capacity, params, device, early_known=False)
         if not (host_k.is_pinned() and host_v.is_pinned()):
             raise TypeError("the host tier needs pinned host tensors")
         dev = self.out.device
-        L, Hkv, P, d = shape.num_layers, shape.num_kv_heads, shape.page_size, shape.head_dim
+        L, Hkv, d = shape.num_layers, shape.num_kv_heads, shape.head_dim
+        hmp = page_table.shape[1] * (P // Ph)
         self.host_k, self.host_v, self.page_table = host_k, host_v, page_table
-        self.hot_k = torch.zeros(L, hot_pages, Hkv, P, d, dtype=torch.bfloat16, device=dev)
+        self.hot_k = torch.zeros(L, hot_pages, Hkv, Ph, d, dtype=torch.bfloat16, device=dev)
         self.hot_v = torch.zeros_like(self.hot_k)
-        self.hot_page_table = torch.full_like(page_table, -1)
+        self.hot_page_table = torch.full((batch, hmp), -1, dtype=torch.int32, device=dev)
         self.hot_owner = torch.full((hot_pages,), -1, dtype=torch.int32, device=dev)
         self.hot_stamp = torch.full((hot_pages,), -1, dtype=torch.int32, device=dev)
-        self.tier_ws = torch.zeros(Z.tier_workspace_bytes(batch, page_table.shape[1], hot_pages), dtype=torch.uint8,
-                                   device=dev)
+        self.tier_ws = torch.zeros(Z.tier_workspace_bytes(batch, hmp, hot_pages), dtype=torch.uint8, device=dev)
         self.lse = torch.zeros(batch, L, shape.num_q_heads, dtype=torch.float32, device=dev)
 
     @property
@@ -58,7 +66,7 @@ class HostTierStep(ZoomrStep):
                            alpha_out=self.alpha, topk_out=self.topk, dev_status=self.status)
         else:
             Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count, self.status)
-        Z.tier_fetch(self.shape, self.host_k, self.host_v, self.page_table, self.hot_k, self.hot_v,
+        Z.tier_fetch(self.host_shape, self.host_k, self.host_v, self.page_table, self.hot_k, self.hot_v,
                      self.hot_page_table, self.hot_owner, self.hot_stamp, self.index, self.count, self.tier_ws,
                      self.status)
         Z.sparse_decode_attn_lse(self.shape, q, self.hot_k, self.hot_v, self.hot_page_table, self.index, self.count,

@@ -96,7 +96,7 @@ def lib():
         L.zoomr_h2o_select.restype = C.c_int
         L.zoomr_tier_workspace_bytes.argtypes = [i32, i32, i32]
         L.zoomr_tier_workspace_bytes.restype = sz
-        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp]
+        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp]
         L.zoomr_tier_fetch.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
@@ -338,18 +338,19 @@ def _host_ptr(t, name):
     return C.c_void_p(t.data_ptr())
 
 
-def tier_workspace_bytes(batch: int, max_pages: int, hot_pages: int) -> int:
-    return int(lib().zoomr_tier_workspace_bytes(int(batch), int(max_pages), int(hot_pages)))
+def tier_workspace_bytes(batch: int, hot_max_pages: int, hot_pages: int) -> int:
+    return int(lib().zoomr_tier_workspace_bytes(int(batch), int(hot_max_pages), int(hot_pages)))
 
 
 def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_table, hot_owner, hot_stamp,
                index, index_count, workspace, dev_status=None, stream=None):
-    """Make the pages of I_f resident in the HBM hot pool (zoomr_tier_fetch). host_k/v: pinned bf16."""
+    """Make the pages of I_f resident in the HBM hot pool (zoomr_tier_fetch). host_k/v: pinned bf16
+    [L][pages][H_kv][P][d] (shape.page_size = P); hot_k/v [L][hot_pages][H_kv][Ph][d]."""
     g = shape.c()
     kv = KV(_host_ptr(host_k, "host_k"), _host_ptr(host_v, "host_v"), host_k.shape[1],
             _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
     rc = lib().zoomr_tier_fetch(C.byref(g), index.shape[0], C.byref(kv), _ptr(hot_k, torch.bfloat16, "hot_k"),
-                                _ptr(hot_v, torch.bfloat16, "hot_v"), hot_k.shape[1],
+                                _ptr(hot_v, torch.bfloat16, "hot_v"), hot_k.shape[1], hot_k.shape[3],
                                 _ptr(hot_page_table, torch.int32, "hot_page_table"),
                                 _ptr(hot_owner, torch.int32, "hot_owner"), _ptr(hot_stamp, torch.int32, "hot_stamp"),
                                 _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),

@@ -59,7 +59,7 @@ class LruModel:
         return len(missing)
 
 
-def _setup_steps(cfg, hot_pages):
+def _setup_steps(cfg, hot_pages, hot_page_size=0):
     from paper_2604_10898_b200 import zoomr as Z
     from paper_2604_10898_b200.step import StepParams, ZoomrStep
     from paper_2604_10898_b200.tier import HostTierStep
@@ -72,16 +72,23 @@ def _setup_steps(cfg, hot_pages):
     ref = ZoomrStep(shape, B, inp.bounds.shape[1], cfg.T, prm, early_known=False)
     ref.update_mean_keys(kv, seg, ref.all_items(inp.num_summaries))
     host_k, host_v = inp.k_pool.cpu().pin_memory(), inp.v_pool.cpu().pin_memory()
-    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, hot_pages)
+    st = HostTierStep(shape, B, inp.bounds.shape[1], cfg.T, prm, host_k, host_v, inp.page_table, hot_pages,
+                      hot_page_size=hot_page_size)
     st.mean_keys.copy_(ref.mean_keys)
     return inp, ref, st, kv, seg
 
 
-@pytest.mark.parametrize("cfg,hot_pages", [(_cfg("b2"), 90), (_cfg("g7_p16", Hq=14, Hkv=2, page=16, seed=72), 170)],
-                         ids=lambda x: x.name if hasattr(x, "name") else str(x))
-def test_tier_steps_equal_hbm_and_follow_lru(cfg, hot_pages):
-    inp, ref, st, kv, seg = _setup_steps(cfg, hot_pages)
-    B, mp, P = inp.q.shape[0], inp.page_table.shape[1], cfg.page
+@pytest.mark.parametrize("cfg,hot_pages,ph", [
+    (_cfg("b2"), 90, 0),
+    (_cfg("g7_p16", Hq=14, Hkv=2, page=16, seed=72), 170, 0),
+    (_cfg("hot16_of_32", seed=73), 170, 16),   # hot pages smaller than host pages
+    (_cfg("hot8_of_32_g1", Hq=2, Hkv=2, seed=74), 330, 8),
+], ids=lambda x: x.name if hasattr(x, "name") else str(x))
+def test_tier_steps_equal_hbm_and_follow_lru(cfg, hot_pages, ph):
+    inp, ref, st, kv, seg = _setup_steps(cfg, hot_pages, ph)
+    B, P = inp.q.shape[0], ph or cfg.page  # P: the hot page size
+    R = cfg.page // P
+    mp = inp.page_table.shape[1] * R
     model = LruModel(hot_pages)
     g = torch.Generator(device="cuda").manual_seed(cfg.seed)
     fetched = []
@@ -107,12 +114,13 @@ def test_tier_steps_equal_hbm_and_follow_lru(cfg, hot_pages):
             want[x] = h
         np.testing.assert_array_equal(hpt, want)
         np.testing.assert_array_equal(st.hot_owner.cpu().numpy(), model.owner)
-        # resident pages hold exactly their host pages (every layer, K and V)
-        pt = inp.page_table.cpu().numpy().reshape(-1)
-        xs = sorted(model.pt)
-        hs = torch.tensor([model.pt[x] for x in xs], device="cuda")
-        ps = torch.tensor([int(pt[x]) for x in xs], device="cuda")
-        assert torch.equal(st.hot_k[:, hs], inp.k_pool[:, ps]) and torch.equal(st.hot_v[:, hs], inp.v_pool[:, ps])
+        # resident pages hold exactly their host rows (every layer, K and V)
+        pt = inp.page_table.cpu().numpy()
+        for x, h in model.pt.items():
+            b, lph = divmod(x, mp)
+            hp, sub = int(pt[b, lph // R]), lph % R
+            for hot, pool in ((st.hot_k, inp.k_pool), (st.hot_v, inp.v_pool)):
+                assert torch.equal(hot[:, h], pool[:, hp, :, sub * P:(sub + 1) * P])
     assert fetched[0] > 0 and sum(fetched[1:]) > 0  # cold start, then churn
     # and one step against the oracle, for good measure
     b = 0

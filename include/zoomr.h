@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 6
+#define ZOOMR_ABI_VERSION 7
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -230,9 +230,17 @@ int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, con
  * a0 -- KV append, Alg.1 @P:407 ("Append k_t and v_t to KV cache"): writes the
  * current token's rows k_new / v_new (bf16 [B][L][H_kv][d]) at position
  * T = seq_len[b] of sequence b (page page_table[b][T / P], slot T % P), then sets
- * seq_len[b] = T + 1.  Device errors: INDEX_RANGE (no page for T). */
+ * seq_len[b] = T + 1.  The pools may be pinned host memory (the host tier's
+ * write-through copy).  Device errors: INDEX_RANGE (no page for T). */
 int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
                     const void *v_new, int32_t *seq_len, int32_t *dev_status, void *stream);
+
+/* The rows of the newest token (position seq_len[b] - 1, already counted) into
+ * another copy of the cache -- the host tier's hot pool after zoomr_tier_fetch
+ * made the page resident (the host copy took it through zoomr_append_kv).
+ * seq_len is not changed.  Device errors: INDEX_RANGE (no page for the position). */
+int zoomr_write_newest_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
+                          const void *v_new, const int32_t *seq_len, int32_t *dev_status, void *stream);
 
 /* Segment tracking from the token just appended (P:19-21 summary delimiters,
  * SPEC ingest_token S:36-45; P:109 semantic boundaries).  token_ids[b] is the id

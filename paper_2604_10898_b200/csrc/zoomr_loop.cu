@@ -17,9 +17,10 @@ namespace zoomr {
 __global__ void append_kv_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
                                  __nv_bfloat16 *kpool, __nv_bfloat16 *vpool, int64_t num_pages,
                                  const int32_t *__restrict__ page_table, int32_t max_pages, int32_t L, int32_t Hkv,
-                                 int32_t P, int32_t d, const int32_t *__restrict__ seq_len_in, int32_t *status) {
+                                 int32_t P, int32_t d, const int32_t *__restrict__ seq_len_in, int32_t back,
+                                 int32_t *status) {
   const int b = blockIdx.y, l = blockIdx.x;
-  const int T = seq_len_in[b];
+  const int T = seq_len_in[b] - back;  // back = 1: the newest token, already counted in seq_len
   const int lp = T / P;
   int page = (T >= 0 && lp < max_pages) ? page_table[(int64_t)b * max_pages + lp] : -1;
   if (page < 0 || page >= num_pages) {
@@ -101,8 +102,22 @@ extern "C" int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoom
   append_kv_kernel<<<dim3(geom->num_layers, batch), 128, 0, s>>>(
       (const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k, (__nv_bfloat16 *)kv->v, kv->num_pages,
       kv->page_table, kv->max_pages, geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, seq_len,
-      dev_status);
+      0, dev_status);
   advance_kernel<<<(batch + 127) / 128, 128, 0, s>>>(seq_len, batch);
+  return launch_status();
+}
+
+extern "C" int zoomr_write_newest_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
+                                     const void *v_new, const int32_t *seq_len, int32_t *dev_status, void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !kv || !kv->k || !kv->v || !kv->page_table || !k_new || !v_new || !seq_len ||
+      kv->num_pages < 1 || kv->max_pages < 1)
+    return ZOOMR_ERR_INVALID_ARG;
+  append_kv_kernel<<<dim3(geom->num_layers, batch), 128, 0, (cudaStream_t)stream>>>(
+      (const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k, (__nv_bfloat16 *)kv->v, kv->num_pages,
+      kv->page_table, kv->max_pages, geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, seq_len,
+      1, dev_status);
   return launch_status();
 }
 

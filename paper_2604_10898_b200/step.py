@@ -158,8 +158,9 @@ class DecodeLoop(ZoomrStep):
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
                  params: StepParams, begin_id: int, end_id: int, boundary_ids, device="cuda",
-                 debug_outputs: bool = False):
-        super().__init__(shape, batch, max_summaries, index_capacity, params, device, debug_outputs)
+                 debug_outputs: bool = False, early_known: bool = True):
+        super().__init__(shape, batch, max_summaries, index_capacity, params, device, debug_outputs,
+                         early_known=early_known)
         dev = torch.device(device)
         self.begin_id, self.end_id = int(begin_id), int(end_id)
         self.boundary_ids = torch.as_tensor(list(boundary_ids), dtype=torch.int32, device=dev)

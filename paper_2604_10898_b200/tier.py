@@ -75,3 +75,69 @@ class HostTierStep(ZoomrStep):
 
     def launches_per_step(self, *args, **kwargs) -> int:
         return 4  # select, plan, copy, a5
+
+
+class TierDecodeLoop(HostTierStep):
+    """Algorithm 1's whole decode step over the host tier, one CUDA-graph replay:
+
+        a0 append k_t, v_t        zoomr_append_kv into the HOST cache (write-through, T += 1)
+        segment tracking          zoomr_track_segments
+        a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
+                                  the host cache; a2/a3 only at semantic boundaries)
+        tier fetch                zoomr_tier_fetch (pages that entered I_f)
+        newest rows -> hot pool   zoomr_write_newest_kv (its page is resident: I_w holds T-1)
+        a5                        zoomr_sparse_decode_attn_lse on the hot pool
+    """
+
+    def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int, params: StepParams,
+                 host_k, host_v, page_table, hot_pages: int, begin_id: int, end_id: int, boundary_ids,
+                 device="cuda", hot_page_size: int = 0):
+        super().__init__(shape, batch, max_summaries, index_capacity, params, host_k, host_v, page_table, hot_pages,
+                         device, hot_page_size)
+        dev = self.out.device
+        self.begin_id, self.end_id = int(begin_id), int(end_id)
+        self.boundary_ids = torch.as_tensor(list(boundary_ids), dtype=torch.int32, device=dev)
+        self.bounds = torch.zeros(batch, max_summaries, 4, dtype=torch.int32, device=dev)
+        self.num_summaries = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.seq_len = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.track_state = torch.zeros(batch, 4, dtype=torch.int32, device=dev)
+        self.close_items = torch.zeros(batch, 2, dtype=torch.int32, device=dev)
+        self.update = torch.zeros(batch, dtype=torch.uint8, device=dev)
+
+    def start(self, prompt_len):
+        """After a prefill of `prompt_len` tokens (already in the host cache): no summaries yet."""
+        n = torch.as_tensor(prompt_len, dtype=torch.int32, device=self.seq_len.device).expand(self.batch)
+        self.seq_len.copy_(n)
+        self.num_summaries.zero_()
+        self.bounds.zero_()
+        self.flags.zero_()
+        self.track_state.copy_(torch.stack([torch.full_like(n, -1), n, n, n], dim=1))
+
+    def start_from(self, bounds, num_summaries, seq_len):
+        """Continue an existing context (its segment table, N_t, T); mean keys must be cached."""
+        self.bounds.copy_(bounds)
+        self.num_summaries.copy_(num_summaries)
+        self.seq_len.copy_(seq_len)
+        self.flags.zero_()
+        last = torch.clamp(num_summaries.long() - 1, min=0)
+        tail = torch.where(num_summaries > 0, bounds[torch.arange(self.batch, device=bounds.device), last, 3],
+                           torch.zeros_like(num_summaries))
+        self.track_state.copy_(torch.stack([torch.full_like(tail, -1), tail, tail, tail], dim=1))
+
+    def decode_step(self, k_new, v_new, q, token_ids):
+        p, hs = self.params, self.host_shape
+        Z.append_kv(hs, self.host_k, self.host_v, self.page_table, k_new, v_new, self.seq_len, self.status)
+        Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
+                         self.num_summaries, self.track_state, self.close_items, self.update, self.status)
+        Z.select_fused(hs, q, self.host_k, self.host_v, self.page_table, self.bounds, self.num_summaries,
+                       self.seq_len, self.close_items, self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags,
+                       self.index, self.count, self.sel_workspace, partial=self.partial,
+                       agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
+                       dev_status=self.status, update=self.update)
+        Z.tier_fetch(hs, self.host_k, self.host_v, self.page_table, self.hot_k, self.hot_v, self.hot_page_table,
+                     self.hot_owner, self.hot_stamp, self.index, self.count, self.tier_ws, self.status)
+        Z.write_newest_kv(self.shape, self.hot_k, self.hot_v, self.hot_page_table, k_new, v_new, self.seq_len,
+                          self.status)
+        Z.sparse_decode_attn_lse(self.shape, q, self.hot_k, self.hot_v, self.hot_page_table, self.index, self.count,
+                                 self.out, self.lse, self.workspace, dev_status=self.status)
+        return self.out

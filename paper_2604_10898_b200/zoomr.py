@@ -26,6 +26,7 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
+           "zoomr_write_newest_kv",
            "zoomr_status_str", "zoomr_abi_version")
 
 
@@ -50,7 +51,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 6  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 7  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -98,6 +99,8 @@ def lib():
         L.zoomr_tier_workspace_bytes.restype = sz
         L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp]
         L.zoomr_tier_fetch.restype = C.c_int
+        L.zoomr_write_newest_kv.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+        L.zoomr_write_newest_kv.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
@@ -155,10 +158,17 @@ class Shape:
                     self.page_size)
 
 
-def _kv(k_pool, v_pool, page_table):
+def _pool_ptr(t, name, host_ok):
+    """A pool's address: a CUDA tensor, or (host_ok) a pinned host tensor read through its unified address."""
+    if host_ok and isinstance(t, torch.Tensor) and not t.is_cuda:
+        return _host_ptr(t, name)
+    return _ptr(t, torch.bfloat16, name)
+
+
+def _kv(k_pool, v_pool, page_table, host_ok=False):
     if k_pool.shape != v_pool.shape or k_pool.dim() != 5:
         raise ValueError("k/v pools must be [L][num_pages][H_kv][P][d]")
-    return KV(_ptr(k_pool, torch.bfloat16, "k_pool"), _ptr(v_pool, torch.bfloat16, "v_pool"),
+    return KV(_pool_ptr(k_pool, "k_pool", host_ok), _pool_ptr(v_pool, "v_pool", host_ok),
               k_pool.shape[1], _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
 
 
@@ -371,7 +381,7 @@ def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summar
                  index_phys=None, update=None):
     """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None
     (entries with i < 0 are skipped); update: uint8 [B] or None (0 = keep the flags)."""
-    g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
+    g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table, host_ok=True), _seg(bounds, num_summaries, seq_len)
     n_close = 0 if close_items is None else close_items.shape[0]
     rc = lib().zoomr_select_fused(
         C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv), C.byref(sg),
@@ -388,12 +398,22 @@ def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summar
 
 
 def append_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_len, dev_status=None, stream=None):
-    """a0 (zoomr_append_kv): rows k_new / v_new bf16 [B][L][H_kv][d] at position seq_len[b]; seq_len += 1."""
-    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    """a0 (zoomr_append_kv): rows k_new / v_new bf16 [B][L][H_kv][d] at position seq_len[b]; seq_len += 1.
+    The pools may be pinned host tensors (the host tier)."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table, host_ok=True)
     rc = lib().zoomr_append_kv(C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"),
                                _ptr(v_new, torch.bfloat16, "v_new"), _ptr(seq_len, torch.int32, "seq_len"),
                                _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_append_kv", rc)
+
+
+def write_newest_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_len, dev_status=None, stream=None):
+    """The newest token's rows at position seq_len[b] - 1 (zoomr_write_newest_kv); seq_len unchanged."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    rc = lib().zoomr_write_newest_kv(C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"),
+                                     _ptr(v_new, torch.bfloat16, "v_new"), _ptr(seq_len, torch.int32, "seq_len"),
+                                     _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_write_newest_kv", rc)
 
 
 def track_segments(token_ids, begin_id, end_id, boundary_ids, seq_len, bounds, num_summaries, state,

@@ -148,3 +148,66 @@ def test_tier_pool_too_small_reports_capacity():
     torch.cuda.synchronize()
     with pytest.raises(Z.ZoomrError):
         st.check_status()
+
+
+@pytest.mark.parametrize("ph", [0, 8])
+def test_tier_decode_loop_equals_hbm_decode_loop(ph):
+    """Algorithm 1's decode loop over the host tier (write-through append, a1 from the host cache,
+    fetch, newest rows into the hot pool) against the all-HBM DecodeLoop on the same token stream:
+    segment table, flags, I_f and outputs identical at every step, eagerly and as graph replays."""
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.step import DecodeLoop, StepParams
+    from paper_2604_10898_b200.tier import TierDecodeLoop
+    from tests.test_gpu_loop import BEGIN, BOUNDARY, END, token_stream
+    B, L, Hq, Hkv, d, P = 2, 2, 8, 2, 64, 16
+    n_p, steps, MS = 40, 120, 16
+    T_max = n_p + steps
+    prm = StepParams(2, 2, 4, 24)
+    gen = torch.Generator(device="cpu").manual_seed(9)
+    pages = (T_max + P - 1) // P
+    k_pool = torch.randn(L, B * pages, Hkv, P, d, generator=gen).bfloat16()
+    v_pool = torch.randn(L, B * pages, Hkv, P, d, generator=gen).bfloat16()
+    page_table = torch.randperm(B * pages, generator=gen).int().view(B, pages).contiguous().cuda()
+    shape = Z.Shape(L, Hq, Hkv, d, P)
+    ref = DecodeLoop(shape, B, MS, T_max, prm, BEGIN, END, BOUNDARY, early_known=False)
+    kv_dev = (k_pool.cuda(), v_pool.cuda(), page_table)
+    tl = TierDecodeLoop(shape, B, MS, T_max, prm, k_pool.pin_memory(), v_pool.pin_memory(), page_table,
+                        hot_pages=B * pages * (P // (ph or P)), begin_id=BEGIN, end_id=END, boundary_ids=BOUNDARY,
+                        hot_page_size=ph)
+    ref.start(n_p)
+    tl.start(n_p)
+    rng = np.random.default_rng(9)
+    toks = torch.tensor([[t] * B for t in token_stream(rng, steps)], dtype=torch.int32, device="cuda")
+    kin = torch.randn(steps, B, L, Hkv, d, device="cuda").bfloat16()
+    vin = torch.randn(steps, B, L, Hkv, d, device="cuda").bfloat16()
+    qs = torch.randn(steps, B, L, Hq, d, device="cuda").bfloat16()
+    half = steps // 2
+    for i in range(half):  # eager
+        ref.decode_step(kv_dev, kin[i], vin[i], qs[i], toks[i])
+        tl.decode_step(kin[i], vin[i], qs[i], toks[i])
+        torch.cuda.synchronize()
+        ref.check_status()
+        tl.check_status()
+        assert torch.equal(tl.seq_len, ref.seq_len) and torch.equal(tl.num_summaries, ref.num_summaries)
+        assert torch.equal(tl.bounds, ref.bounds) and torch.equal(tl.flags, ref.flags)
+        assert torch.equal(tl.count, ref.count) and torch.equal(tl.index, ref.index)
+        assert torch.equal(tl.out, ref.out), i
+    assert int(tl.num_summaries.min()) >= 1
+    # the rest as graph replays (inputs copied into static buffers)
+    sk, sv, sq, st_ = kin[0].clone(), vin[0].clone(), qs[0].clone(), toks[0].clone()
+    graphs = []
+    for loop, args in ((ref, (kv_dev, sk, sv, sq, st_)), (tl, (sk, sv, sq, st_))):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            loop.decode_step(*args)
+        graphs.append(g)
+    for i in range(half, steps):
+        sk.copy_(kin[i]); sv.copy_(vin[i]); sq.copy_(qs[i]); st_.copy_(toks[i])
+        graphs[0].replay()
+        graphs[1].replay()
+        torch.cuda.synchronize()
+        ref.check_status()
+        tl.check_status()
+        assert torch.equal(tl.index, ref.index) and torch.equal(tl.out, ref.out), i
+    # the host cache received every appended row (write-through)
+    assert torch.equal(tl.host_k.cuda(), kv_dev[0]) and torch.equal(tl.host_v.cuda(), kv_dev[1])

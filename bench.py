@@ -17,6 +17,7 @@ Prints ONE JSON line on rank 0 (bench contract in the task statement).
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -47,6 +48,8 @@ def parse():
     ap.add_argument("--no-early", action="store_true",
                     help="A/B only: a5 waits for I_f before attending I_p / I_w")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--batch-per-gpu", type=int, default=0,
+                    help="sequences per rank (default: the workload's batch split over the ranks)")
     return ap.parse_args()
 
 
@@ -424,6 +427,17 @@ def run_ours(args):
         raise SystemExit("bench.py (ours) needs a CUDA device")
     _build.build()
     cfg = S.config_by_name(args.workload)
+    # batch sharding: the workload's batch is split over the ranks (configs[2]: 64 sequences
+    # over 1..8 GPUs), or --batch-per-gpu fixes the per-rank share
+    from paper_2604_10898_b200.parallel import shard_range
+    lo, hi = shard_range(cfg.batch, rank, world)
+    per_rank = args.batch_per_gpu or max(1, hi - lo)
+    if per_rank != cfg.batch:
+        cfg = dataclasses.replace(cfg, batch=per_rank)
+    kv_bytes = 2 * cfg.batch * cfg.T * cfg.L * cfg.Hkv * cfg.d * 2 * max(1, args.rotate)
+    if torch.cuda.is_available() and kv_bytes > 0.85 * torch.cuda.get_device_properties(local).total_memory:
+        raise SystemExit(f"{cfg.name}: {cfg.batch} sequences per GPU x {args.rotate} input sets need "
+                         f"{kv_bytes / 1e9:.0f} GB of KV; use more GPUs, --batch-per-gpu or --rotate")
     U = max(1, cfg.update_every)
     R = max(1, args.rotate)
     shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
@@ -637,7 +651,7 @@ def run_ours(args):
     if world == 1 and not args.no_loop:
         token_sharded = token_shard_section(shape, prm, sets[0], cfg, K)
     host_tier = None
-    if world == 1 and not args.no_loop:
+    if world == 1 and not args.no_loop and sets[0]["inp"].k_pool.numel() * 4 <= (8 << 30):  # pins the cache
         host_tier = host_tier_section(shape, prm, sets[0], cfg, K)
     # per-stage breakdown (informational): each stage alone, graph-replayed
     stages = {}

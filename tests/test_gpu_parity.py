@@ -133,6 +133,27 @@ def test_many_summaries_histogram_topc(fused):
 
 
 @pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("c,small_group", [(60, True), (300, False)])
+def test_large_tie_group_at_the_topc_cut(c, small_group, fused):
+    """N_t = 1600 with diffuse queries (V = 128 voters, k = 8): most voted summaries
+    hold one or two votes, so the threshold bin of a3 holds a large tie group,
+    ranked by (v desc, A desc, i asc).  c = 60 puts the cut in a group of a few
+    hundred members; c = 300 puts it in the v = 1 group (> 512 members)."""
+    cfg = S.Config("ties1600", L=4, Hq=32, Hkv=8, d=32, T=20480, n_pairs=1600, LR=8, LS=4, sink=16,
+                   window=64, c=c, top_k=8, page=32, seed=21, query="diffuse", off_target=1.0)
+    inp = S.generate(cfg, device="cuda")
+    st = PY.make_step(inp)
+    PY.run_full(inp, st, fused=fused)
+    PY.check_sequence(inp, st, 0, {})
+    # the case asked for: size of the tie group at the cut (votes from the oracle-checked partial)
+    v = st.partial[0, 0, :cfg.n_pairs].cpu()
+    vs = torch.sort(v[v > 0], descending=True).values
+    cut_v = int(vs[min(c, len(vs)) - 1])
+    m = int((v == cut_v).sum())
+    assert len(vs) > c and (m <= 512) == small_group, (len(vs), cut_v, m)
+
+
+@pytest.mark.parametrize("fused", [False, True])
 def test_degenerate_cases(fused):
     """c = 0 (SumR-like keep-all-voted), k > N_t, c > |I_all|, window >= T, sink > T."""
     import dataclasses

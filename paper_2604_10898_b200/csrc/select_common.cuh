@@ -382,7 +382,7 @@ static __device__ void block_topc(const int *v, const long long *A, int nt, int 
 // (see zoomr_index.cu).  fl may live in shared or global memory.
 // One pass reads the segment table (validation + clipped piece extents into
 // shared memory), a block scan turns lengths into offsets, and the fill reads
-// only shared memory: one warp per piece, coalesced stores.
+// only shared memory: coalesced stores (a shuffle search over 32 pieces per warp).
 // With `phys` non-null, also writes the page-resolved row of every entry,
 // phys[j] = pt[t/P] * HkvP + t%P (HkvP = H_kv*P), so that a5 needs no page-table
 // lookup: row(l, g, t) = (l*num_pages*H_kv + g)*P + phys.  `pt` is the sequence's
@@ -436,42 +436,51 @@ static __device__ void block_build_index(const int32_t *__restrict__ bd /* [nt][
     if (count > cap) set_status(status, ZOOMR_ERR_CAPACITY);
     *count_out = count < cap ? count : cap;
   }
-  // Fill: thread t writes the contiguous output positions [t*E, (t+1)*E): one
-  // binary search for its first piece, then a walk that keeps the current piece
-  // in registers (shared memory is touched again only at a piece boundary).
-  // Output layout: [0, s') ++ pieces ++ [w0, T).
+  // Fill, every store coalesced.  Output layout: [0, s') ++ pieces ++ [w0, T).
+  // Sink and window: positions strided over the block.  Pieces: warp w takes
+  // groups of 32 consecutive pieces (lane l holds piece g0 + l's start and
+  // offset); the group's output positions go 32 at a time, one per lane, and a
+  // 5-step shuffle search over the lanes' offsets finds the piece of each.
   const int lim = count < cap ? count : cap;
-  const int E = (lim + (int)blockDim.x - 1) / (int)blockDim.x;
-  int j = tid * E;
-  const int j1 = min(lim, j + E);
   const int wbase = sp + total;
-  const int *off = piece + nt;  // exclusive offsets of the clipped pieces
-  int i = 0;
-  if (nt > 0 && j < j1 && j < wbase && j1 > sp) {  // last piece with off <= max(j - sp, 0)
-    const int r = j > sp ? j - sp : 0;
-    int lo = 0, hi = nt - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (off[mid] <= r) lo = mid; else hi = mid - 1;
+  for (int j = tid; j < sp && j < lim; j += blockDim.x) emit(j, j);                   // sink
+  for (int j = wbase + tid; j < lim; j += blockDim.x) emit(j, w0 + (j - wbase));      // window
+  const int lane = tid & 31, warp = tid >> 5, nwarp = ((int)blockDim.x + 31) >> 5;
+  const int *off = piece + nt;  // exclusive offsets of the clipped pieces (relative to s')
+  const int pend = min(total, lim - sp);  // piece positions [0, pend) are written
+  const int Ew = ((pend + nwarp - 1) / nwarp + 127) & ~127;
+  const int c1 = min(pend, (warp + 1) * Ew);
+  int cur = warp * Ew;
+  if (nt > 0 && cur < c1) {
+    int bi = 0, hi = nt - 1;  // the window's first piece: last piece with offset <= cur
+    while (bi < hi) {
+      const int mid = (bi + hi + 1) >> 1;
+      if (off[mid] <= cur) bi = mid; else hi = mid - 1;
     }
-    i = lo;
-  }
-  int pc_start = nt ? piece[i] : 0, pc_off = nt ? off[i] : 0;
-  int pc_end = (i + 1 < nt) ? off[i + 1] : total;
-  for (; j < j1; ++j) {
-    if (j < sp) {
-      emit(j, j);  // sink
-    } else if (j < wbase) {
-      const int r = j - sp;
-      while (r >= pc_end) {  // next non-empty piece
-        ++i;
-        pc_start = piece[i];
-        pc_off = off[i];
-        pc_end = (i + 1 < nt) ? off[i + 1] : total;
+    while (cur < c1) {
+      const int i = bi + lane;
+      const int my_off = i < nt ? off[i] : total;
+      const int my_start = i < nt ? piece[i] : 0;
+      const int wend = min(c1, bi + 32 < nt ? off[bi + 32] : total);
+      for (; cur < wend; cur += 128) {  // warp-uniform: 4 positions per lane in flight
+        int L[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int o = __shfl_sync(0xffffffffu, my_off, L[u] + st);
+            if (o <= cur + 32 * u + lane) L[u] += st;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = cur + 32 * u + lane;
+          const int ps = __shfl_sync(0xffffffffu, my_start, L[u]), po = __shfl_sync(0xffffffffu, my_off, L[u]);
+          if (r < wend) emit(sp + r, ps + (r - po));
+        }
       }
-      emit(j, pc_start + (r - pc_off));
-    } else {
-      emit(j, w0 + (j - wbase));  // window
+      cur = wend;
+      bi += 32;
     }
   }
 }

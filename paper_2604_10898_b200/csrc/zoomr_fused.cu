@@ -65,7 +65,7 @@ struct FusedParams {
 };
 
 template <int D, int G>
-__global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) {
+__global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
   allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
@@ -177,15 +177,40 @@ __global__ void __launch_bounds__(256) fused_select_kernel(const FusedParams p) 
     for (int x = threadIdx.x; x < p.max_pages; x += blockDim.x) pts[x] = p.page_table[(int64_t)b * p.max_pages + x];
   // collect the aggregate (leaving the accumulators zeroed for the next call)
   // and stage the segment table for a4; without an update, the held flags
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-    bds[i] = reinterpret_cast<const int4 *>(bd)[i];
-    if (upd) {
-      v[i] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
-      A[i] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
-      p.ws_votes[(int64_t)b * MS + i] = 0;
-      p.ws_a[(int64_t)b * MS + i] = 0;
-    } else {
-      fl[i] = p.flags[(int64_t)b * MS + i];
+  // (kCU entries per thread per round, every load issued before the stores:
+  // one round trip per round instead of one per entry)
+  constexpr int kCU = 4;
+  for (int i0 = threadIdx.x; i0 < nt; i0 += kCU * blockDim.x) {
+    int4 bq[kCU];
+    int vq[kCU];
+    long long aq[kCU];
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nt) {
+        bq[u] = reinterpret_cast<const int4 *>(bd)[i];
+        if (upd) {
+          vq[u] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
+          aq[u] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
+        } else {
+          vq[u] = p.flags[(int64_t)b * MS + i];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nt) {
+        bds[i] = bq[u];
+        if (upd) {
+          v[i] = vq[u];
+          A[i] = aq[u];
+          p.ws_votes[(int64_t)b * MS + i] = 0;
+          p.ws_a[(int64_t)b * MS + i] = 0;
+        } else {
+          fl[i] = (uint8_t)vq[u];
+        }
+      }
     }
   }
   __syncthreads();

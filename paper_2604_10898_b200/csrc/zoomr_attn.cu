@@ -47,6 +47,9 @@ constexpr int kTile = 32;   // tokens per tile (one per lane when resolving addr
 constexpr int kPairs = 4;   // producer/consumer warp pairs per CTA
 constexpr int kStages = 3;  // ring depth per pair
 constexpr int kPtSmem = 4096; // page-table entries staged in shared memory when they fit
+#ifndef ZOOMR_MERGE_STAGE
+#define ZOOMR_MERGE_STAGE 1  // last-flush merges read the parts through the idle ring (A/B: -DZOOMR_MERGE_STAGE=0)
+#endif
 
 template <int D>
 struct AttnShape {
@@ -784,6 +787,22 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       }
 #pragma unroll
       for (int u = 0; u < PER; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // At the warp's last flush the pair's ring is idle: stage every other part
+      // into it (after this warp's own part) with all copies in flight at once --
+      // one L2 round trip for the whole merge instead of one per NPF parts.
+      float *stg = own + SLOT;
+      const bool staged = ZOOMR_MERGE_STAGE && at_end && (nparts + 1) * SLOT * 4 <= kStages * S::STAGE_BYTES;
+      if (staged) {
+        __syncwarp();  // a previous merge's shared-memory reads are done
+        for (int j = 0; j < nparts; ++j) {
+          if (j == own_j) continue;
+          const float *qp = part_ptr(xb, xs, j, wf0, n0w, wf1);
+          const uint32_t dst = smem_u32(stg + j * SLOT);
+          for (int c = lane; c < SLOT / 4; c += 32) cp_async16(dst + 16 * c, qp + 4 * c, 16);
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+      }
       for (int j0 = 0; j0 < nparts; j0 += NPF) {
         float mh[NPF][G], lh[NPF][G];
         float4 ov4[NPF][PER];
@@ -799,6 +818,18 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
             for (int u = 0; u < PER; ++u) {
               const int f = lane + 32 * u;
               ov4[j][u] = f < NV4 ? reinterpret_cast<const float4 *>(own + HDR)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          } else if (j0 + j < nparts && staged) {  // staged in shared memory
+            const float *qp = stg + (j0 + j) * SLOT;
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              mh[j][h] = qp[h];
+              lh[j][h] = qp[G + h];
+            }
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+              const int f = lane + 32 * u;
+              ov4[j][u] = f < NV4 ? reinterpret_cast<const float4 *>(qp + HDR)[f] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           } else if (j0 + j < nparts) {
             const float *qp = part_ptr(xb, xs, j0 + j, wf0, n0w, wf1);

@@ -571,6 +571,37 @@ def run_ours(args):
     h2d = sets[0]["inp"].q.numel() * 2
     d2h = sets[0]["st"].out.numel() * 4
 
+    # Steps enqueued back to back (a serving loop capturing several steps per
+    # graph): R x 4 full steps in one graph, plain launches vs the chained ones
+    # (zoomr_select_fused_chained runs a1/a2 while the previous step's a5
+    # finishes).  Informational: `value` stays one step per graph replay.
+    chained = None
+    if U == 1:
+        def multi_graph(flag):
+            for s in sets:
+                s["st"].chained = flag
+            gm_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gm_):
+                for _ in range(4):
+                    for s in sets:
+                        s["st"].run(s["inp"].q, s["kv"], s["seg"], close_items=s["newest"])
+            for s in sets:
+                s["st"].chained = False
+            return gm_
+        g_plain, g_chain = multi_graph(False), multi_graph(True)
+        n_multi = max(1, K // (4 * R))
+        t_plain = max_over_ranks(timed(lambda i: g_plain.replay(), n_multi, 2), world) / (n_multi * 4 * R)
+        t_chain = max_over_ranks(timed(lambda i: g_chain.replay(), n_multi, 2), world) / (n_multi * 4 * R)
+        for s in sets:
+            s["g"].replay()  # leave each set's one-step state in place
+        torch.cuda.synchronize()
+        for s in sets:
+            s["st"].check_status()
+        chained = {"steps_per_graph": 4 * R, "plain_us_per_step": t_plain * 1e6, "chained_us_per_step": t_chain * 1e6,
+                   "chained_seqs_per_s": world * Bseq / t_chain,
+                   "note": "zoomr_select_fused_chained + zoomr_sparse_decode_attn_chained: a1/a2 of step t+1 "
+                           "overlap the end of step t's a5 (PDL); outputs bit-identical (tests/test_gpu_paths.py)"}
+
     # Algorithm 1's whole decode step on the device (append, segment tracking,
     # selection update at semantic boundaries only, I_f rebuild, attention):
     # one graph replay per token over the last 256 positions of a context,
@@ -719,6 +750,7 @@ def run_ours(args):
                      "launch_us": attn_s * 1e6},
         "stages_us": stages,
         "decode_loop": decode_loop,
+        "chained": chained,
         "policies": policies,
         "token_sharded": token_sharded,
         "host_tier": host_tier,

@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 7
+#define ZOOMR_ABI_VERSION 8
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -224,6 +224,38 @@ int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, con
                        int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
                        int32_t *topk_out, void *workspace, size_t workspace_bytes,
                        int32_t *dev_status, void *stream);
+
+/* Chained launches across decode steps (ABI 8).  Same arguments, semantics and
+ * bit-identical outputs as zoomr_sparse_decode_attn / zoomr_select_fused; only
+ * the launch overlap differs:
+ *   zoomr_sparse_decode_attn_chained lets a successor launched with
+ *   programmatic dependent launch start as soon as every CTA finished its
+ *   prologue, i.e. during the tail of this launch (its end spread);
+ *   zoomr_select_fused_chained is launched with PDL and runs a1 + a2 (mean
+ *   keys, scoring, the per-voter top-k and the vote atomics) before
+ *   griddepcontrol.wait, and a3 + a4 (writing partial / flags / index / count)
+ *   after it, when the predecessor has completed and its writes are visible.
+ * Contract: the kernel preceding zoomr_select_fused_chained on the stream writes
+ * none of a1/a2's inputs (q, the pools, page table, segment table, seq_len,
+ * close_items, update, mean keys) -- normally it is the previous step's
+ * zoomr_sparse_decode_attn_chained, which reads index / count and writes only
+ * out and its own workspace; and the kernel following a chained a5 must not be
+ * a PDL-launched zoomr_sparse_decode_attn* using the same workspace. */
+int zoomr_sparse_decode_attn_chained(const zoomr_geom *geom, int32_t batch, const void *q,
+                                     const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                     const int32_t *index_count, int32_t index_capacity,
+                                     const int32_t *seq_len, int32_t sink, int32_t window,
+                                     float softmax_scale, float *out, void *workspace,
+                                     size_t workspace_bytes, int32_t *dev_status, void *stream);
+
+int zoomr_select_fused_chained(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                               const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                               const uint8_t *update,
+                               float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
+                               int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
+                               int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                               int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                               int32_t *dev_status, void *stream);
 
 /* ---- Algorithm 1's per-token bookkeeping, on device ----------
  *

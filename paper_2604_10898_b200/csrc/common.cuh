@@ -60,9 +60,9 @@ inline void prefer_max_smem(F *kfn) {
 // its predecessor on the stream is finishing; it must execute
 // `griddepcontrol.wait` before touching the predecessor's outputs.
 template <typename Kern, typename... Args>
-inline void launch_pdl(Kern kfn, int grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+inline void launch_pdl(Kern kfn, dim3 grid, int block, size_t smem, cudaStream_t stream, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;

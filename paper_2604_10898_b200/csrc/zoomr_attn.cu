@@ -96,6 +96,7 @@ struct AttnParams {
   int32_t *ws_cnt; // [B*L*Hkv]
   int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
   int32_t pt_smem;               // page table staged in shared memory (B*max_pages <= kPtSmem)
+  int32_t early_trigger;         // chained: a PDL-launched successor may start after this CTA's prologue
   float scale_log2;
   const int32_t *seq_len;  // nullable: with it, I_p and I_w are attended before the wait (phase A)
   int32_t sink, window;
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   __syncthreads();
 
   if (threadIdx.x == 0) TL(1);
+  if (p.early_trigger) allow_dependents();
   const int64_t NW = (int64_t)gridDim.x * kPairs;
   const int pair = warp % kPairs;
   const bool producer = warp >= kPairs;
@@ -1142,7 +1144,7 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
                               const int32_t *index, const int32_t *index_phys, const int32_t *index_count,
                               int32_t index_capacity, const int32_t *seq_len, int32_t sink, int32_t window,
                               float softmax_scale, float *out, float *lse, void *workspace, size_t workspace_bytes,
-                              int32_t *dev_status, void *stream, float *logits = nullptr) {
+                              int32_t *dev_status, void *stream, float *logits = nullptr, bool chained = false) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !q || !kv || !kv->k || !kv->v || !kv->page_table || !index || !index_count ||
@@ -1182,6 +1184,7 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   for (int sft = 0; sft < 31; ++sft)
     if ((1 << sft) == geom->page_size) prm.Pshift = sft;
   prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+  prm.early_trigger = chained ? 1 : 0;
   prm.seq_len = seq_len;
   prm.sink = sink;
   prm.window = window;
@@ -1235,6 +1238,17 @@ extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, c
                                         size_t workspace_bytes, int32_t *dev_status, void *stream) {
   return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
                             softmax_scale, out, nullptr, workspace, workspace_bytes, dev_status, stream);
+}
+
+extern "C" int zoomr_sparse_decode_attn_chained(const zoomr_geom *geom, int32_t batch, const void *q,
+                                                const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                                const int32_t *index_count, int32_t index_capacity,
+                                                const int32_t *seq_len, int32_t sink, int32_t window,
+                                                float softmax_scale, float *out, void *workspace,
+                                                size_t workspace_bytes, int32_t *dev_status, void *stream) {
+  return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
+                            softmax_scale, out, nullptr, workspace, workspace_bytes, dev_status, stream, nullptr,
+                            true);
 }
 
 extern "C" int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,

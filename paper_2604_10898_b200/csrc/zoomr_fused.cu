@@ -60,6 +60,7 @@ struct FusedParams {
   int32_t L, Hkv, P;
   int32_t *status;
   int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
+  int32_t pdl_front;  // chained: launched with PDL after a5; a1/a2 run before griddepcontrol.wait, a3/a4 after
   int32_t designated_tail;  // the grid is resident at once: the last-launched CTA of b runs a3/a4
   const uint8_t *update;    // nullable: update[b] == 0 keeps b's flags (no a2/a3; a1 and a4 still run)
 };
@@ -68,7 +69,7 @@ template <int D, int G>
 __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
-  allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
+  if (!p.pdl_front) allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
   TL_INIT();
   TL(0);
   const int lg = blockIdx.x, b = blockIdx.y;
@@ -159,6 +160,10 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   }
   __syncthreads();
   if (!ticket_last) return;
+  }
+  if (p.pdl_front) {  // the predecessor (a5) reads index / count: wait for it before a3/a4 write them
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    allow_dependents();
   }
   if (threadIdx.x == 0) TL(2);
   if (p.stop_after == 1) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
@@ -266,14 +271,14 @@ extern "C" size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t b
   return (size_t)batch * max_summaries * (8 + 4) + (size_t)batch * 4 + 256;
 }
 
-extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
-                                  const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
-                                  const uint8_t *update,
-                                  float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
-                                  int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
-                                  int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
-                                  int32_t *topk_out, void *workspace, size_t workspace_bytes,
-                                  int32_t *dev_status, void *stream) {
+static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                        const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                        const uint8_t *update,
+                        float *mean_keys, int32_t top_k, int32_t c, int32_t sink, int32_t window,
+                        int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
+                        int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
+                        int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                        int32_t *dev_status, void *stream, bool chained) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !q || !kv || !kv->k || !kv->page_table || !seg || !seg->bounds || !seg->num_summaries ||
@@ -318,6 +323,7 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   p.Hkv = geom->num_kv_heads;
   p.P = geom->page_size;
   p.status = dev_status;
+  p.pdl_front = chained ? 1 : 0;
   {
     const char *e = getenv("ZOOMR_FUSED_STOP");
     p.stop_after = e ? atoi(e) : 0;
@@ -335,7 +341,8 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
     int per_sm = 0;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);                      \
     p.designated_tail = (int64_t)grid.x * grid.y <= (int64_t)per_sm * num_sms();                \
-    kfn<<<grid, 256, smem, s>>>(p);                                                              \
+    if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                            \
+    else kfn<<<grid, 256, smem, s>>>(p);                                                         \
   } while (0)
 #define ZOOMR_FS_G(DD)               \
   switch (G) {                       \
@@ -356,3 +363,17 @@ extern "C" int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const v
   return launch_status();
 }
 
+#define ZOOMR_SELECT_FUSED_ARGS                                                                                 \
+  const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv, const zoomr_segments *seg,          \
+      const int32_t *close_items, int32_t n_close, const uint8_t *update, float *mean_keys, int32_t top_k,      \
+      int32_t c, int32_t sink, int32_t window, int64_t *partial, uint8_t *flags, float *agreeability,           \
+      int32_t *index, int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,     \
+      int32_t *topk_out, void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream
+#define ZOOMR_SELECT_FUSED_CALL(CH)                                                                            \
+  select_fused(geom, batch, q, kv, seg, close_items, n_close, update, mean_keys, top_k, c, sink, window,        \
+               partial, flags, agreeability, index, index_phys, index_capacity, index_count, alpha_out,        \
+               topk_out, workspace, workspace_bytes, dev_status, stream, CH)
+
+extern "C" int zoomr_select_fused(ZOOMR_SELECT_FUSED_ARGS) { return ZOOMR_SELECT_FUSED_CALL(false); }
+
+extern "C" int zoomr_select_fused_chained(ZOOMR_SELECT_FUSED_ARGS) { return ZOOMR_SELECT_FUSED_CALL(true); }

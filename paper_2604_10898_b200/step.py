@@ -29,8 +29,11 @@ class ZoomrStep:
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
                  params: StepParams, device="cuda", debug_outputs: bool = False, use_phys: bool = False,
-                 early_known: bool = True):
+                 early_known: bool = True, chained: bool = False):
         self.shape, self.batch, self.params = shape, batch, params
+        # steps enqueued back to back (several per CUDA graph): the fused select of
+        # step t+1 runs a1/a2 while a5 of step t finishes (zoomr_*_chained)
+        self.chained = chained
         self.max_summaries, self.cap = max_summaries, index_capacity
         dev = torch.device(device)
         L, Hq, Hkv, d = shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
@@ -90,8 +93,9 @@ class ZoomrStep:
                            self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags, self.index,
                            self.count, self.sel_workspace, partial=self.partial,
                            agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
-                           dev_status=self.status, index_phys=self.index_phys if self.use_phys else None)
-            self.attend(q, kv, seq_len)
+                           dev_status=self.status, index_phys=self.index_phys if self.use_phys else None,
+                           chained=self.chained)
+            self.attend(q, kv, seq_len, chained=self.chained)
             return self.out
         if close_items is not None and close_items.numel():
             self.update_mean_keys(kv, seg, close_items)
@@ -106,7 +110,7 @@ class ZoomrStep:
         self.attend(q, kv, seq_len, phys=False)
         return self.out
 
-    def attend(self, q, kv, seq_len, phys=None):
+    def attend(self, q, kv, seq_len, phys=None, chained=False):
         """a5 over the current I_f.  With early_known, I_p and I_w (known from
         T alone) are attended while the producer of I_f is still running."""
         k_pool, v_pool, page_table = kv
@@ -115,7 +119,8 @@ class ZoomrStep:
         Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
                              self.out, self.workspace, dev_status=self.status,
                              index_phys=self.index_phys if use_phys else None,
-                             seq_len=seq_len if self.early_known else None, sink=p.sink, window=p.window)
+                             seq_len=seq_len if self.early_known else None, sink=p.sink, window=p.window,
+                             chained=chained)
 
     def launches_per_step(self, update_selection=True, close=False, fused=True) -> int:
         """Kernel launches one run() enqueues (a2 = zero + score when not fused)."""

@@ -26,7 +26,7 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
-           "zoomr_write_newest_kv",
+           "zoomr_write_newest_kv", "zoomr_sparse_decode_attn_chained", "zoomr_select_fused_chained",
            "zoomr_status_str", "zoomr_abi_version")
 
 
@@ -51,7 +51,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 7  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 8  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -230,14 +230,17 @@ def attn_workspace_bytes(shape: Shape, batch: int) -> int:
 
 def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out,
                        workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
-                       seq_len=None, sink=0, window=0):
+                       seq_len=None, sink=0, window=0, chained=False):
     """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once.
+    chained: zoomr_sparse_decode_attn_chained (a PDL-launched successor, normally
+    select_fused(chained=True) of the next step, may start during this launch).
 
     seq_len/sink/window (optional): `index` is a4's output for these values, so
     I_p and I_w are attended before the kernel waits for I_f (see zoomr.h)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
-    rc = lib().zoomr_sparse_decode_attn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
+    fn = lib().zoomr_sparse_decode_attn_chained if chained else lib().zoomr_sparse_decode_attn
+    rc = fn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
                                         C.byref(kv), _ptr(index, torch.int32, "index"),
                                         _ptr(index_phys, torch.int32, "index_phys"),
                                         _ptr(index_count, torch.int32, "index_count"), index.shape[1],
@@ -378,12 +381,14 @@ def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:
 def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summaries, seq_len, close_items,
                  mean_keys, top_k, c, sink, window, flags, index, index_count, workspace, partial=None,
                  agreeability=None, alpha_out=None, topk_out=None, dev_status=None, stream=None,
-                 index_phys=None, update=None):
+                 index_phys=None, update=None, chained=False):
     """a1+a2+a3+a4 in one launch (zoomr_select_fused). close_items: int32 [n][2] or None
-    (entries with i < 0 are skipped); update: uint8 [B] or None (0 = keep the flags)."""
+    (entries with i < 0 are skipped); update: uint8 [B] or None (0 = keep the flags).
+    chained: zoomr_select_fused_chained -- the preceding kernel on the stream is a
+    chained a5 (or writes none of a1/a2's inputs); a1/a2 overlap its end."""
     g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table, host_ok=True), _seg(bounds, num_summaries, seq_len)
     n_close = 0 if close_items is None else close_items.shape[0]
-    rc = lib().zoomr_select_fused(
+    rc = (lib().zoomr_select_fused_chained if chained else lib().zoomr_select_fused)(
         C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv), C.byref(sg),
         _ptr(close_items, torch.int32, "close_items") if n_close else None, n_close,
         _ptr(update, torch.uint8, "update"), _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k), int(c), int(sink), int(window),

@@ -151,3 +151,64 @@ def test_comparison_policies(policy, cfg_name):
             o = oracle.attend_one(q[l, h], np.ascontiguousarray(Kr[:, 0, h // G]), np.ascontiguousarray(Vr[:, 0, h // G]),
                                   np.arange(len(idx)))
             assert np.abs(out[l, h] - o).max() <= 2e-3
+
+
+@pytest.mark.parametrize("cfg", [
+    _small("chain_b3", d=128, batch=3),
+    _small("chain_g7", d=128, Hq=14, Hkv=2),
+    dataclasses.replace(S.CONFIGS["8b16k"], seed=12),
+], ids=lambda c: c.name)
+def test_chained_steps_in_one_graph(cfg):
+    """zoomr_select_fused_chained / zoomr_sparse_decode_attn_chained (ABI 8): several
+    steps over independent input sets captured back to back in ONE graph, each
+    select running a1/a2 while the previous step's a5 finishes.  Every step's
+    outputs are bit-identical to the same step run alone (unchained), and the
+    small cases are checked against the oracle."""
+    from paper_2604_10898_b200 import zoomr as Z
+    R = 3
+    sets = []
+    for r in range(R):
+        inp = S.generate(cfg, device="cuda", seed=cfg.seed + 5 * r)
+        cap = 8192 if cfg.T > 4096 else None
+        ref, st = PY.make_step(inp, capacity=cap), PY.make_step(inp, capacity=cap)
+        st.chained = True
+        PY.run_full(inp, ref, fused=True)  # unchained, eager
+        kv = (inp.k_pool, inp.v_pool, inp.page_table)
+        seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+        st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+        newest = torch.tensor([[b, int(n) - 1] for b, n in enumerate(inp.num_summaries.cpu().tolist())],
+                              dtype=torch.int32, device="cuda")
+        sets.append((inp, ref, st, kv, seg, newest))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up (kernel attributes) outside the capture
+        for inp, ref, st, kv, seg, newest in sets:
+            st.run(inp.q, kv, seg, close_items=newest)
+    torch.cuda.current_stream().wait_stream(s)
+    with torch.cuda.graph(g):
+        for _ in range(3):
+            for inp, ref, st, kv, seg, newest in sets:
+                st.run(inp.q, kv, seg, close_items=newest)
+    for _, _, st, *_ in sets:
+        st.out.zero_()
+        st.index.zero_()
+        st.count.zero_()
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+    for inp, ref, st, kv, seg, newest in sets:
+        st.check_status()
+        ref.check_status()
+        assert torch.equal(st.count, ref.count)
+        for b in range(inp.q.shape[0]):
+            n = int(st.count[b])
+            assert torch.equal(st.index[b, :n], ref.index[b, :n])
+        assert torch.equal(st.flags, ref.flags)
+        assert torch.equal(st.out, ref.out)
+        if cfg.T <= 4096:
+            rep = {}
+            for b in range(inp.q.shape[0]):
+                PY.check_sequence(inp, st, b, rep)
+    assert "zoomr_select_fused_chained" in Z.EXPORTS

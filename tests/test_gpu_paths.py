@@ -211,4 +211,13 @@ def test_chained_steps_in_one_graph(cfg):
             rep = {}
             for b in range(inp.q.shape[0]):
                 PY.check_sequence(inp, st, b, rep)
+    # a plain a5 enqueued right behind a chained one on the same workspace
+    # attends index-only (the early rows would race the chained launch's merges)
+    inp, ref, st, kv, seg, newest = sets[0]
+    for _ in range(3):
+        st.run(inp.q, kv, seg, close_items=newest)
+        st.attend(inp.q, kv, inp.seq_len)
+    torch.cuda.synchronize()
+    st.check_status()
+    assert (st.out - ref.out).abs().max().item() <= 1e-5
     assert "zoomr_select_fused_chained" in Z.EXPORTS

@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-early", action="store_true",
                     help="A/B only: a5 waits for I_f before attending I_p / I_w")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] batch-64 section")
+    ap.add_argument("--no-heads", action="store_true", help="skip the configs[3] head-sharded section")
     ap.add_argument("--batch-per-gpu", type=int, default=0,
                     help="sequences per rank (default: the workload's batch split over the ranks)")
     return ap.parse_args()
@@ -155,23 +157,83 @@ def barrier(world):
         dist.barrier()
 
 
+def per_step_us(fn, K, W):
+    """Per-step GPU times (us) from a CUDA event pair around each step (a separate
+    pass from the headline timing, so the extra event records do not touch it)."""
+    for i in range(W):
+        fn(i)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i in range(K):
+        ev[i][0].record()
+        fn(i)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) * 1e3 for a, b in ev]
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = (len(xs) - 1) * q
+    lo, hi = int(k), min(int(k) + 1, len(xs) - 1)
+    return xs[lo] + (xs[hi] - xs[lo]) * (k - lo)
+
+
+def pcts(xs):
+    return {"p10": pct(xs, 0.1), "p50": pct(xs, 0.5), "p90": pct(xs, 0.9)}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # --------------------------------------------------------------- CPU oracle --
-def oracle_time(inp, seconds, threads=0):
-    """Time the CPU oracle (as it stands) on rank 0: full steps of sequence 0."""
-    import oracle
+def oracle_inputs(inp, b=0):
     from zoomr_synth import bf16_bits, logical_rows
+    K = bf16_bits(logical_rows(inp, b, "k"))
+    V = bf16_bits(logical_rows(inp, b, "v"))
+    q = bf16_bits(inp.q[b])
+    n = int(inp.num_summaries[b])
+    seg = inp.bounds[b, :n].cpu().numpy()
+    return q, K, V, seg
+
+
+def oracle_full_step(cfg, x, threads=0):
+    """One full oracle step (O1-O7: a1-a5 over every layer and head) of one sequence."""
+    import oracle
+    q, K, V, seg = x
+    return oracle.step(q, K, V, seg, cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.top_k, cfg.c, cfg.sink, cfg.window,
+                       threads=threads)
+
+
+def oracle_time(inp, seconds, threads=0):
+    """Time the CPU oracle (as it stands) on rank 0: full steps of sequence 0, for
+    about `seconds` (the cpu_baseline leg; the reference arm times the same
+    function step by step)."""
+    import oracle
     oracle.build()
     cfg = inp.cfg
-    K = bf16_bits(logical_rows(inp, 0, "k"))
-    V = bf16_bits(logical_rows(inp, 0, "v"))
-    q = bf16_bits(inp.q[0])
-    n = int(inp.num_summaries[0])
-    seg = inp.bounds[0, :n].cpu().numpy()
+    x = oracle_inputs(inp)
     nth = oracle.num_threads(threads)
     steps, t0 = 0, time.perf_counter()
     while True:
-        oracle.step(q, K, V, seg, cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.top_k, cfg.c, cfg.sink, cfg.window,
-                    threads=threads)
+        oracle_full_step(cfg, x, threads)
         steps += 1
         el = time.perf_counter() - t0
         if el >= seconds:
@@ -179,68 +241,59 @@ def oracle_time(inp, seconds, threads=0):
     return steps, el, nth
 
 
+def oracle_tiny_single_thread():
+    """configs[0] (tiny) on ONE host thread: best of 3 full oracle steps, us."""
+    import zoomr_synth as S
+    inp = S.generate(S.CONFIGS["tiny"], device="cpu")
+    x = oracle_inputs(inp)
+    best = None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle_full_step(inp.cfg, x, threads=1)
+        el = (time.perf_counter() - t0) * 1e6
+        best = el if best is None else min(best, el)
+    return best
+
+
 def run_reference(args):
-    """Reference arm = the CPU oracle (there is no reference implementation to
-    install: /root/reference holds only the paper and a spec).  Each timed step is
-    a bounded sample of the workload: the full selection (a1-a4 over all layers
-    and voters) plus attention for a rotating 1/8 of the layers; the reported
-    seqs/s extrapolates the sampled attention to all layers."""
+    """Reference arm = the CPU oracle as it stands (there is no reference
+    implementation to install: /root/reference holds only the paper and a spec).
+    Each step is one FULL oracle step (O1-O7: the whole selection and the
+    attention of every layer and head) of one sequence of the workload -- the
+    same function the cpu_baseline leg of our arm times.  Under torchrun only
+    rank 0 runs it."""
     rank, world, local = init_dist(args.gpus)
     if rank != 0:
         return
-    import numpy as np
     import zoomr_synth as S
+    import oracle
+    oracle.build()
     cfg = S.config_by_name(args.workload)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    inp = S.generate(cfg, device=dev, query_mode=args.query)
-    import oracle
-    from zoomr_synth import bf16_bits, logical_rows
-    oracle.build()
-    K = bf16_bits(logical_rows(inp, 0, "k"))
-    V = bf16_bits(logical_rows(inp, 0, "v"))
-    q = bf16_bits(inp.q[0])
-    n = int(inp.num_summaries[0])
-    seg = inp.bounds[0, :n].cpu().numpy()
-    T = K.shape[0]
-    frac = 8
-    per = max(1, cfg.L // frac)
-    t_sel = t_att = 0.0
-    count = 0
-
-    def one(i):
-        nonlocal t_sel, t_att, count
+    inp = S.generate(cfg, device=dev, batch=1, query_mode=args.query)
+    x = oracle_inputs(inp)
+    for _ in range(args.warmup):
+        r = oracle_full_step(cfg, x)
+    times = []
+    for _ in range(args.steps):
         t0 = time.perf_counter()
-        mk = oracle.update_mean_keys(K, seg, cfg.L, cfg.Hkv, cfg.d)
-        sc = oracle.score(q, mk, cfg.top_k, cfg.L, cfg.Hq, cfg.Hkv, cfg.d)
-        flags, _, _ = oracle.select_topc(sc["votes"], sc["A"], cfg.c)
-        idx = oracle.build_index(seg, flags, T, cfg.sink, cfg.window)
-        t1 = time.perf_counter()
-        l0 = (i * per) % cfg.L
-        ls = slice(l0, l0 + per)
-        oracle.sparse_decode_attn(np.ascontiguousarray(q[ls]), np.ascontiguousarray(K[:, ls]),
-                                  np.ascontiguousarray(V[:, ls]), idx, per, cfg.Hq, cfg.Hkv, cfg.d)
-        t2 = time.perf_counter()
-        count = len(idx)
-        return t1 - t0, t2 - t1
-    for i in range(args.warmup):
-        one(i)
-    for i in range(args.steps):
-        a, b = one(i)
-        t_sel += a
-        t_att += b
-    step_s = (t_sel + t_att * cfg.L / per) / args.steps
-    val = inp.q.shape[0] / step_s
+        r = oracle_full_step(cfg, x)
+        times.append(time.perf_counter() - t0)
+    step_s = sum(times) / len(times)
+    val = 1.0 / step_s
     cores = oracle.num_threads(0)
-    sample = (f"per step: full a1-a4 selection over all {cfg.L}x{cfg.Hq} voters + a5 attention for {per} of "
-              f"{cfg.L} layers (rotating), extrapolated to all layers; one {cfg.name} sequence")
+    sample = (f"per step: one full oracle step (a1-a5, all {cfg.L}x{cfg.Hq} heads) of one {cfg.name} sequence "
+              f"(zoomr_oracle_step, fp64, OpenMP over (layer, head)); seqs/s = 1 / mean step time")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "seqs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "batch": inp.q.shape[0], "T": cfg.T, "n_summaries": n,
-                   "index_count": int(count), "query": args.query},
-        "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "config": {"workload": cfg.name, "batch": 1, "T": cfg.T, "n_summaries": int(inp.num_summaries[0]),
+                   "index_count": int(len(r["index"])), "query": args.query},
+        "step_ms_pcts": {k: v * 1e3 for k, v in pcts(times).items()},
+        "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "seqs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -309,6 +362,138 @@ def token_shard_section(shape, prm, s0, cfg, K, world_sim=8):
             "max_abs_diff_vs_unsharded": err,
             "note": "ranks simulated one after another on one GPU; each rank: a2+a3+a4 (replicated) + "
                     "shard_index + a5 with lse over its part of I_f; NVLink all-gather not included"}
+
+
+def c3_section(rank, world, K, W, hbm):
+    """BASELINE configs[2]: Llama-3-8B shape, 32K context, batch 64, batch-sharded
+    over the ranks (64 / N sequences each, no collective).  When a rank's share of
+    the KV does not fit its HBM (N = 1: 275 GB), logical pages alias onto a smaller
+    physical pool by a seeded hash: the bytes read per step are
+    unchanged, and the pool (~1000x L2) gives no cross-sequence L2 reuse."""
+    import zoomr_synth as S
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.parallel import shard_range
+    from paper_2604_10898_b200.step import StepParams, ZoomrStep
+    cfg = S.CONFIGS["8b32k"]
+    lo, hi = shard_range(cfg.batch, rank, world)
+    nb = hi - lo
+    page_bytes = 2 * cfg.L * cfg.Hkv * cfg.page * cfg.d * 2
+    need_pages = nb * cfg.pages_per_seq
+    free = torch.cuda.mem_get_info()[0]
+    budget = free - (24 << 30)  # mean keys, index, workspaces, generator temporaries
+    phys = None if need_pages * page_bytes <= budget else max(1, int(budget // page_bytes))
+    inp = S.generate(cfg, device="cuda", seed=cfg.seed + 1000 * rank, batch=nb, phys_pages=phys)
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    st = ZoomrStep(shape, nb, inp.bounds.shape[1], cfg.T, StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window))
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    newest = torch.tensor([[b, int(n) - 1] for b, n in enumerate(inp.num_summaries.cpu().tolist())],
+                          dtype=torch.int32, device="cuda")
+    g = st.capture(inp.q, kv, seg, close_items=newest)
+    ga = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(ga):
+        st.attend(inp.q, kv, inp.seq_len)
+    g.replay()
+    torch.cuda.synchronize()
+    st.check_status()
+    Kc = max(5, min(K, 30))
+    barrier(world)
+    ts = per_step_us(lambda i: g.replay(), Kc, max(2, min(W, 5)))
+    ta = per_step_us(lambda i: ga.replay(), Kc, 2)
+    st.check_status()
+    counts = [int(c) for c in st.count.cpu()]
+    nsum = [int(n) for n in inp.num_summaries.cpu()]
+    by = algorithmic_bytes(cfg, counts, nsum, closures=nb)
+    step_us = statistics.median(ts)
+    step_max = max_over_ranks(step_us, world)
+    a5_us = statistics.median(ta)
+    res = {"workload": "8b32k (configs[2])", "global_batch": cfg.batch, "ranks": world, "batch_per_rank": nb,
+           "aliased_phys_pages": phys, "logical_pages": need_pages,
+           "kv_gb_per_rank": (phys or need_pages) * page_bytes / 1e9,
+           "step_us_median": step_us, "step_us_pcts": pcts(ts), "step_us_max_over_ranks": step_max,
+           "seqs_per_s": cfg.batch / (step_max * 1e-6),
+           "bytes_per_step": by["total"], "step_frac_of_hbm_peak": by["total"] / (step_us * 1e-6) / 1e9 / hbm,
+           "a5_us_median": a5_us, "a5_frac_of_hbm_peak": by["a5"] / (a5_us * 1e-6) / 1e9 / hbm,
+           "index_count_mean": sum(counts) / len(counts), "timing": "median of per-replay CUDA events, "
+           f"{Kc} replays; seqs/s = 64 / max over ranks"}
+    del st, inp, g, ga
+    torch.cuda.empty_cache()
+    return res
+
+
+def head_sharded_section(rank, world, K, W, hbm):
+    """BASELINE configs[3]: Llama-3-70B shape, 64K context, batch 1, KV-head-sharded
+    (SURVEY 8(e).2): each rank owns 8 / N KV heads and their query heads for all 80
+    layers; a1, a2 and a5 are local; ONE NCCL all-reduce(SUM) of the int64
+    `partial` (votes, fixed-point A) sits between a2 and a3, captured in the CUDA
+    graph with the step.  At N = 1 this is a dry run of rank 0 of an 8-way split
+    over a 1-rank NCCL communicator (the all-reduce kernel runs, but no NVLink
+    transfer).  Reported with and without the all-reduce, at U = 1 / 16 / 64."""
+    import socket
+    import torch.distributed as dist
+    import zoomr_synth as S
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.parallel import nccl_allreduce_sum
+    from paper_2604_10898_b200.step import StepParams, ZoomrStep
+    full = S.CONFIGS["70b64k"]
+    n_sh = 8 if world == 1 else world
+    if full.Hkv % n_sh:
+        return {"skipped": f"{n_sh} ranks do not divide H_kv = {full.Hkv}"}
+    own_group = False
+    if world == 1 and not dist.is_initialized():
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        own_group = True
+    # the rank's heads, generated at that size (same distribution as a slice of the full model)
+    cfg = dataclasses.replace(full, Hq=full.Hq // n_sh, Hkv=full.Hkv // n_sh)
+    inp = S.generate(cfg, device="cuda", seed=full.seed + 100 * rank)
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    st = ZoomrStep(shape, 1, inp.bounds.shape[1], cfg.T, StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window))
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    newest = torch.tensor([[0, int(inp.num_summaries[0]) - 1]], dtype=torch.int32, device="cuda")
+    ar = nccl_allreduce_sum()
+    g_ar = st.capture(inp.q, kv, seg, close_items=newest, allreduce=ar, fused=False)
+    g_no = st.capture(inp.q, kv, seg, close_items=newest, fused=False)
+    g_light = st.capture(inp.q, kv, seg, update_selection=False)
+    g_ar.replay()
+    torch.cuda.synchronize()
+    st.check_status()
+    Kc = max(10, min(K, 100))
+    barrier(world)
+    t_ar = per_step_us(lambda i: g_ar.replay(), Kc, max(3, min(W, 10)))
+    t_no = per_step_us(lambda i: g_no.replay(), Kc, 3)
+    t_li = per_step_us(lambda i: g_light.replay(), Kc, 3)
+    st.check_status()
+    m_ar, m_no, m_li = statistics.median(t_ar), statistics.median(t_no), statistics.median(t_li)
+    m_ar_max = max_over_ranks(m_ar, world)
+    cnt = int(st.count[0])
+    by = algorithmic_bytes(cfg, [cnt], [int(inp.num_summaries[0])])
+    res = {"workload": "70b64k (configs[3])", "shards": n_sh, "ranks_executed": world,
+           "heads_per_rank": {"H_kv": cfg.Hkv, "H_q": cfg.Hq, "L": cfg.L},
+           "communicator": "NCCL, world 1 (dry run: the all-reduce kernel, no transfer)" if world == 1
+           else f"NCCL, world {world}",
+           "allreduce_bytes": int(st.partial.numel() * 8), "index_count": cnt,
+           "step_us_U1_with_allreduce": m_ar, "step_us_U1_with_allreduce_pcts": pcts(t_ar),
+           "step_us_U1_with_allreduce_max_over_ranks": m_ar_max,
+           "step_us_U1_without_allreduce": m_no, "allreduce_us": m_ar - m_no,
+           "step_us_held_selection": m_li,
+           "step_us_U16": (m_ar + 15 * m_li) / 16, "step_us_U64": (m_ar + 63 * m_li) / 64,
+           "seqs_per_s_U1": 1e6 / m_ar_max,
+           "bytes_per_step_per_rank": by["total"],
+           "step_frac_of_hbm_peak_U1": by["total"] / (m_ar * 1e-6) / 1e9 / hbm,
+           "path": "separate a1 / a2 / all-reduce / a3 / a4 / a5 launches (the fused select has no all-reduce "
+                   "point); U = 16 / 64 = one update step + U-1 held-selection steps (a4 + a5)"}
+    del st, inp, g_ar, g_no, g_light
+    torch.cuda.empty_cache()
+    if own_group:
+        dist.destroy_process_group()
+    return res
 
 
 def host_tier_section(shape, prm, s0, cfg, K, hot_page_sizes=(64, 16)):
@@ -503,6 +688,7 @@ def run_ours(args):
             timed(step_fn, K, 0)
     clk.__exit__()
     t_step_max = max_over_ranks(t_step, world)
+    step_times = per_step_us(step_fn, K, W)  # p10 / p50 / p90 (separate pass)
     t_attn = timed(lambda i: sets[i % R]["ga"].replay(), K, W)
     bytes_mean = sum((per_set_bytes if is_full(i) else light_set_bytes)[i % R]["total"] for i in range(K)) / K
     a5_mean = sum(per_set_bytes[i % R]["a5"] for i in range(K)) / K
@@ -613,14 +799,32 @@ def run_ours(args):
         inp0 = s0["inp"]
         n_tok = 256
         start = inp0.seq_len - n_tok
-        lp = DecodeLoop(shape, Bseq, inp0.bounds.shape[1], cfg.T, prm, 1000, 1001, [200])
-        lp.mean_keys.copy_(s0["st"].mean_keys)
+        nmax0 = inp0.bounds.shape[1]
+        extra = 8  # room for the summaries that close during the stretch
+        lp = DecodeLoop(shape, Bseq, nmax0 + extra, cfg.T, prm, 1000, 1001, [200])
+        lp.mean_keys[:, :, :, :nmax0].copy_(s0["st"].mean_keys)
         # the closed summaries must end before the appended stretch (the bench context keeps its
         # open tail > 256 tokens, so they do)
-        lp.start_from(inp0.bounds, inp0.num_summaries, start)
+        bpad = torch.zeros(Bseq, nmax0 + extra, 4, dtype=torch.int32, device="cuda")
+        bpad[:, :nmax0] = inp0.bounds
+        lp.start_from(bpad, inp0.num_summaries, start)
         kin = torch.randn(Bseq, cfg.L, cfg.Hkv, cfg.d, device="cuda").bfloat16()
         vin = torch.randn_like(kin)
-        toks = [200 if (i % 35) == 34 else 7 for i in range(n_tok)]
+        # the token stream: regular text with a sentence boundary every 35 tokens,
+        # and every LR+LS tokens a summary (begin delimiter, LS-2 summary tokens, end
+        # delimiter): each end closes a summary (a1 on closure, N_t grows), so
+        # selection updates see N_t = 120, 121, ...
+        toks = []
+        for i in range(n_tok):
+            r = i % (cfg.LR + cfg.LS)
+            if r == cfg.LR:
+                toks.append(1000)
+            elif r == cfg.LR + cfg.LS - 1:
+                toks.append(1001)
+            elif (i % 35) == 34:
+                toks.append(200)
+            else:
+                toks.append(7)
         tok_dev = torch.tensor([[t] * Bseq for t in toks], dtype=torch.int32, device="cuda")
         gl_ = torch.cuda.CUDAGraph()  # all n_tok decode steps in one graph (5 launches each)
         with torch.cuda.graph(gl_):
@@ -639,8 +843,10 @@ def run_ours(args):
         loop_run()
         us = loop_run()
         lp.check_status()
+        n_closed = int(lp.num_summaries[0]) - int(inp0.num_summaries[0])
         decode_loop = {"us_per_token": us, "tokens": n_tok, "selection_updates": sum(t == 200 for t in toks),
-                       "launches_per_token": 5, "note": "append + segment tracking + fused select (a2/a3 at "
+                       "summaries_closed": n_closed, "launches_per_token": 5,
+                       "note": "append + segment tracking + fused select (a1 at summary closures, a2/a3 at "
                        "sentence boundaries only) + a5; the 256 steps captured in one CUDA graph"}
     # the paper's comparison policies on the same kernels (NEXT-3), informational:
     # StreamingLLM at ZoomR's budget (mean |I_f|), SumR (all summaries kept): a4 + a5 per step;
@@ -720,6 +926,11 @@ def run_ours(args):
         s["st"].check_status()
 
     hbm, peak_src = peaks()
+    # configs[2] (batch 64, batch-sharded, aliased pages when a rank's share does not
+    # fit) and configs[3] (70B-64K KV-head-sharded with the NCCL all-reduce in the
+    # graph; a 1-rank dry run at N = 1) -- sections of the same line
+    c3 = None if args.no_c3 else c3_section(rank, world, K, W, hbm)
+    head_sharded = None if args.no_heads else head_sharded_section(rank, world, K, W, hbm)
     step_s = t_step_max / K
     value = world * Bseq * K / t_step_max
     attn_s = t_attn / K
@@ -742,6 +953,7 @@ def run_ours(args):
                    "l2": f"inputs larger than L2: {R} independent input sets rotated per step, "
                          f"each step reads {bytes_mean / 1e6:.0f} MB"},
         "step_us": step_s * 1e6,
+        "step_us_pcts": pcts(step_times),
         "step_roofline": {"bytes_per_step": bytes_mean, "achieved_gbs": bytes_mean / step_s / 1e9,
                           "frac": bytes_mean / step_s / 1e9 / hbm},
         "roofline": {"kernel": "a5 zoomr_sparse_decode_attn", "bound": "hbm", "achieved": achieved,
@@ -754,6 +966,8 @@ def run_ours(args):
         "policies": policies,
         "token_sharded": token_sharded,
         "host_tier": host_tier,
+        "c3": c3,
+        "head_sharded": head_sharded,
         "e2e": {"value": world * Bseq * K / t_e2e, "unit": "seqs/s", "pipelined": True,
                 "serial_value": world * Bseq * K / t_e2e_serial, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
@@ -764,7 +978,8 @@ def run_ours(args):
         steps, el, nth = oracle_time(sets[0]["inp"], args.cpu_seconds)
         line["cpu_baseline"] = {"value": steps * Bseq / el, "unit": "seqs/s", "cores": nth, "kind": "oracle",
                                 "sample": f"{steps} full oracle steps (a1-a5, all {cfg.L}x{cfg.Hq} heads) of "
-                                          f"one {cfg.name} sequence, {el:.1f} s"}
+                                          f"one {cfg.name} sequence, {el:.1f} s",
+                                "cpu_model": cpu_model(), "tiny_single_thread_us": oracle_tiny_single_thread()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

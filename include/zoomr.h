@@ -23,9 +23,12 @@
  *
  * Conventions shared by every call
  *  - Ownership: every array argument is DEVICE memory allocated and owned by
- *    the caller.  The library never allocates device memory, never frees or
- *    retains a pointer past the call, and has no global mutable state.  Host
- *    structs (zoomr_geom, zoomr_kv, zoomr_segments) are read during the call only.
+ *    the caller.  The library never allocates device memory and never frees or
+ *    retains a pointer past the call.  Its only host state is, per stream, the
+ *    kind of its own most recent launch (a small mutex-protected table): it is
+ *    what lets a chained call detect an unsafe predecessor and fall back to
+ *    the serialised launch (see "Chained launches").  Host structs
+ *    (zoomr_geom, zoomr_kv, zoomr_segments) are read during the call only.
  *  - Streams: `stream` is a cudaStream_t (passed as void*); all work is
  *    enqueued on it asynchronously; no call synchronizes the host.  Every call
  *    is CUDA-graph capturable.  Concurrent calls on different streams are safe
@@ -51,7 +54,7 @@
 extern "C" {
 #endif
 
-#define ZOOMR_ABI_VERSION 8
+#define ZOOMR_ABI_VERSION 9
 
 typedef enum {
   ZOOMR_OK = 0,
@@ -161,7 +164,8 @@ int zoomr_build_index(int32_t batch, const zoomr_segments *seg, const uint8_t *f
                       int32_t *index_count, int32_t *dev_status, void *stream);
 
 /* Workspace for a5: split-K partial results and per-(b,l,g) arrival counters.
- * Must be zero-filled once before the first call; every call leaves it zeroed. */
+ * Must be zero-filled once before the first call; every call leaves it zeroed.
+ * Independent of layer_begin / layer_count: one workspace serves every layer range. */
 size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
 
 /* a5 -- sparse GQA decode attention over I_f, P:74 and P:145-149:
@@ -173,6 +177,13 @@ size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
  * (page_table[t/P]*H_kv*P + t%P); when given, the page table is not read.
  * softmax_scale is normally 1/sqrt(d).
  *
+ * layer_begin, layer_count: attend layers [layer_begin,
+ * layer_begin + layer_count) only -- a model calls a5 once per layer, and the
+ * host-memory tier pipelines the per-layer fetch against it.  q, out
+ * and the pools keep their full [.][L][..] layout; out rows of other layers
+ * are not written.  layer_count = 0 means "through the last layer"; a range
+ * outside [0, L) is INVALID_ARG.
+ *
  * seq_len (nullable, int32 [B], device) + sink + window: when given, I_f MUST
  * be a4's output for the same T = seq_len[b], sink and window, i.e. start with
  * I_p = [0, min(sink, T)) and end with I_w = [max(min(sink, T), T - window), T)
@@ -180,16 +191,18 @@ size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t batch);
  * from T alone -- before it waits for the producer of I_f (it is launched with
  * programmatic dependent launch), so that part of the gather overlaps the
  * selection; the rest of I_f is read from `index` afterwards.  Only this
- * kernel's workspace is written before the wait, so the kernel preceding it on
- * the stream must not be another zoomr_sparse_decode_attn call that uses the
- * same workspace (normally it is zoomr_select_fused or zoomr_build_index).  NULL: every row comes from
+ * kernel's workspace is written before the wait.  If the library's previous
+ * launch on this stream was a chained a5 on the same workspace (which may still
+ * be merging from it), the call detects it and attends index-only instead (as
+ * if seq_len were NULL): no caller rule to keep.  NULL: every row comes from
  * `index` (any sorted or unsorted list of positions is then accepted). */
 int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
                              const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                              const int32_t *index_count, int32_t index_capacity,
                              const int32_t *seq_len, int32_t sink, int32_t window,
-                             float softmax_scale, float *out, void *workspace,
-                             size_t workspace_bytes, int32_t *dev_status, void *stream);
+                             float softmax_scale, int32_t layer_begin, int32_t layer_count,
+                             float *out, void *workspace, size_t workspace_bytes,
+                             int32_t *dev_status, void *stream);
 
 /* a1 + a2 + a3 + a4 fused into ONE launch for the single-rank / batch-sharded
  * step (Algorithm 1's selection).  Same semantics and bit-identical
@@ -225,28 +238,35 @@ int zoomr_select_fused(const zoomr_geom *geom, int32_t batch, const void *q, con
                        int32_t *topk_out, void *workspace, size_t workspace_bytes,
                        int32_t *dev_status, void *stream);
 
-/* Chained launches across decode steps (ABI 8).  Same arguments, semantics and
- * bit-identical outputs as zoomr_sparse_decode_attn / zoomr_select_fused; only
- * the launch overlap differs:
+/* Chained launches across decode steps (ABI 8; ABI 9 made the ordering
+ * self-checking).  Same arguments, semantics and bit-identical outputs as
+ * zoomr_sparse_decode_attn / zoomr_select_fused; only the launch overlap differs:
  *   zoomr_sparse_decode_attn_chained lets a successor launched with
- *   programmatic dependent launch start as soon as every CTA finished its
- *   prologue, i.e. during the tail of this launch (its end spread);
- *   zoomr_select_fused_chained is launched with PDL and runs a1 + a2 (mean
- *   keys, scoring, the per-voter top-k and the vote atomics) before
+ *   programmatic dependent launch start as soon as every CTA has passed its
+ *   griddepcontrol.wait -- so after this launch's own predecessor (the select
+ *   that wrote I_f) has completed -- i.e. during this launch's streaming and
+ *   end spread;
+ *   zoomr_select_fused_chained, when the library's previous launch on the
+ *   stream is a chained a5, is launched with PDL and runs a1 + a2 (mean keys,
+ *   scoring, the per-voter top-k and the vote atomics) before
  *   griddepcontrol.wait, and a3 + a4 (writing partial / flags / index / count)
- *   after it, when the predecessor has completed and its writes are visible.
- * Contract: the kernel preceding zoomr_select_fused_chained on the stream writes
- * none of a1/a2's inputs (q, the pools, page table, segment table, seq_len,
- * close_items, update, mean keys) -- normally it is the previous step's
- * zoomr_sparse_decode_attn_chained, which reads index / count and writes only
- * out and its own workspace; and the kernel following a chained a5 must not be
- * a PDL-launched zoomr_sparse_decode_attn* using the same workspace. */
+ *   after it, when that a5 has completed and its writes are visible.  After
+ *   any other launch it runs exactly like zoomr_select_fused.
+ * So two selects on the same workspace never overlap (select(t+1) starts after
+ * a5(t) passed its wait, which is after select(t) completed), and an a5 never
+ * writes its workspace while a chained a5 on it may still run (detected above).
+ * Remaining caller rule: a FOREIGN kernel enqueued between a chained a5 and
+ * zoomr_select_fused_chained must not write a1/a2's inputs (q, the pools, page
+ * table, segment table, seq_len, close_items, update, mean keys) after
+ * triggering its own dependents early -- the library cannot see foreign
+ * launches.  Launched without PDL (the common case) such a kernel is safe. */
 int zoomr_sparse_decode_attn_chained(const zoomr_geom *geom, int32_t batch, const void *q,
                                      const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                      const int32_t *index_count, int32_t index_capacity,
                                      const int32_t *seq_len, int32_t sink, int32_t window,
-                                     float softmax_scale, float *out, void *workspace,
-                                     size_t workspace_bytes, int32_t *dev_status, void *stream);
+                                     float softmax_scale, int32_t layer_begin, int32_t layer_count,
+                                     float *out, void *workspace, size_t workspace_bytes,
+                                     int32_t *dev_status, void *stream);
 
 int zoomr_select_fused_chained(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
                                const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
@@ -319,12 +339,14 @@ int zoomr_shard_index(int32_t batch, const int32_t *index, const int32_t *index_
  * with index_count 0 is skipped: its out and lse rows are left untouched (the
  * merge below excludes it through part_count).  Nothing is read before the
  * preceding kernel on the stream has completed -- the page table included, so
- * it may be that kernel's output (zoomr_tier_fetch's residency table). */
+ * it may be that kernel's output (zoomr_tier_fetch's residency table).
+ * layer_begin / layer_count as for zoomr_sparse_decode_attn (lse rows of other
+ * layers untouched): the host tier attends layer by layer behind its fetch. */
 int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
                                  const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                  const int32_t *index_count, int32_t index_capacity, float softmax_scale,
-                                 float *out, float *lse, void *workspace, size_t workspace_bytes,
-                                 int32_t *dev_status, void *stream);
+                                 int32_t layer_begin, int32_t layer_count, float *out, float *lse,
+                                 void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
 
 /* Combine n_parts partial attention results (normally the all-gathered outputs
  * of zoomr_sparse_decode_attn_lse on each rank, over disjoint index sets):

@@ -28,9 +28,25 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-inline int launch_status() {
+// The library's only host state: per stream, the kind of its own most recent
+// launch (and the a5 workspace it used).  It lets a call detect, at enqueue
+// time, the one launch order whose overlap would be unsafe -- a PDL-launched
+// a5 that writes its workspace before griddepcontrol.wait, enqueued right
+// behind a chained a5 on the same workspace -- and fall back to the
+// serialised variant instead of racing (zoomr.h "Chained launches").  Stream
+// order is enqueue order, also under graph capture, so the record is exact for
+// the library's own launches; a foreign kernel in between only makes the
+// fallback conservative.  A stale entry (a destroyed stream whose handle is
+// reused) can likewise only cause a conservative fallback.
+enum LaunchKind : int { kLaunchOther = 0, kLaunchA5Chained = 1 };
+void note_launch(cudaStream_t s, int kind, const void *ws);
+bool prev_launch_is(cudaStream_t s, int kind, const void *ws);  // ws == nullptr: any workspace
+
+inline int launch_status(cudaStream_t s, int kind = kLaunchOther, const void *ws = nullptr) {
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? ZOOMR_OK : ZOOMR_ERR_CUDA;
+  if (e != cudaSuccess) return ZOOMR_ERR_CUDA;
+  note_launch(s, kind, ws);
+  return ZOOMR_OK;
 }
 
 inline int num_sms() {
@@ -76,6 +92,23 @@ inline void launch_pdl(Kern kfn, dim3 grid, int block, size_t smem, cudaStream_t
   }
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 0 : 1;
+  cudaLaunchKernelEx(&cfg, kfn, args...);
+}
+
+// Cooperative launch: the whole grid is co-resident (the launch fails if it
+// cannot be), which kernels whose CTAs wait on one another require.
+template <typename Kern, typename... Args>
+inline void launch_cooperative(Kern kfn, dim3 grid, int block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kfn, args...);
 }
 

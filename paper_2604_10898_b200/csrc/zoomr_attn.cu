@@ -36,6 +36,8 @@
 //    transposed into the PV B-operand with movmatrix.
 //  * fp32 online softmax (exp2 with scale*log2e folded in), fp32 output.
 #include <cuda.h>  // CUtensorMap (the encode entry point is fetched through the runtime)
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -94,9 +96,10 @@ struct AttnParams {
   float *logits;   // kLogits only: s_j = q . k_j * scale per (b, l, h, index position) (H2O)
   float *ws_part;  // [2][NW + B*L*Hkv][SLOT]: partial of (phase, warp w, segment s) at [phase][w + s]
   int32_t *ws_cnt; // [B*L*Hkv]
-  int32_t B, L, Hkv, P, Pshift;  // Pshift = log2(P) when P is a power of two, else -1
+  int32_t B, L, Hkv, P, Pshift;  // L: layers of q / out / the pools; Pshift = log2(P) when P is a power of two, else -1
+  int32_t l0, Lc;                // this launch attends layers [l0, l0 + Lc) (a model's per-layer call)
   int32_t pt_smem;               // page table staged in shared memory (B*max_pages <= kPtSmem)
-  int32_t early_trigger;         // chained: a PDL-launched successor may start after this CTA's prologue
+  int32_t early_trigger;         // chained: a PDL-launched successor may start once this CTA passed its wait
   float scale_log2;
   const int32_t *seq_len;  // nullable: with it, I_p and I_w are attended before the wait (phase A)
   int32_t sink, window;
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   // barriers) as warp-uniform, which keeps the TMA issue's operands in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int Hq = p.Hkv * G;
-  const int LH = p.L * p.Hkv;
+  const int LH = p.Lc * p.Hkv;  // segments (b, layer in [l0, l0 + Lc), KV head) per sequence
   TL_INIT();
   if (threadIdx.x == 0) {
     TL(0);
@@ -318,7 +321,6 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   __syncthreads();
 
   if (threadIdx.x == 0) TL(1);
-  if (p.early_trigger) allow_dependents();
   const int64_t NW = (int64_t)gridDim.x * kPairs;
   const int pair = warp % kPairs;
   const bool producer = warp >= kPairs;
@@ -371,6 +373,12 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       if (lane == 0) prefB[p.B] = carry;
       __syncwarp();
       if (lane == 0) mbar_arrive(bready);  // release: the schedule above is visible to the waiters
+      // Chained: the successor (normally the next step's fused select) may launch
+      // once every CTA got here, i.e. after griddepcontrol.wait -- so after this
+      // launch's own predecessor (the select writing I_f, and the select's
+      // workspace) has completed.  Triggering any earlier would let select(t+1)
+      // touch the shared selection workspace while select(t) still runs.
+      if (p.early_trigger) allow_dependents();
     } else {
       mbar_wait(bready, 0, 7);  // acquire (suspends instead of hammering shared memory)
     }
@@ -431,8 +439,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       a.b = wk.b;
       const int seg = wk.seg, tis = wk.tis;
       const int4 in = info[a.b];
-      a.l = seg / p.Hkv;
-      a.g = seg - a.l * p.Hkv;
+      const int sl = seg / p.Hkv;
+      a.l = p.l0 + sl;
+      a.g = seg - sl * p.Hkv;
       const int pos = tis * kTile + lane;
       if (a.ph == 0) {  // [0, s') ++ [w0, T)
         a.ok = pos < in.z;
@@ -691,7 +700,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       seg_parts(b, seg, wf0, n0w, wf1, n1w);
       final_out = n0w + n1w == 1;
       if (final_out) {  // this warp is the segment's only part: final output
-        const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+        const int sl = seg / p.Hkv, g = seg - sl * p.Hkv, l = p.l0 + sl;
         float *ob = p.out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
         if (owner) {
           const float inv0 = 1.f / l0, inv1 = 1.f / l1;
@@ -775,7 +784,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       __syncwarp();  // the other lanes' partial loads below are ordered after lane 0's acquire
       // last arriver: online merge of the parts in a fixed order (deterministic),
       // NPF parts per round with all their loads in flight
-      const int xl = xs / p.Hkv, xg = xs - xl * p.Hkv;
+      const int xsl = xs / p.Hkv, xg = xs - xsl * p.Hkv, xl = p.l0 + xsl;
       float *ob = p.out + (((int64_t)xb * p.L + xl) * Hq + (int64_t)xg * G) * D;
       constexpr int NV4 = G * D / 4;
       constexpr int PER = (NV4 + 31) / 32;
@@ -937,7 +946,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       cur_b = b;
       cur_seg = seg;
       // Q fragments (B operand of QK^T): Q[head n % G][k-chunk], this thread's column n = gq
-      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      const int sl = seg / p.Hkv, g = seg - sl * p.Hkv, l = p.l0 + sl;
       const __nv_bfloat16 *qh = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G + (gq % G)) * D;
 #pragma unroll
       for (int ks = 0; ks < NKS; ++ks) {
@@ -991,7 +1000,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       cm1 = fmaxf(cm1, fmaxf(sacc[mt][1], sacc[mt][3]));
     }
     if constexpr (kLogits) {  // H2O: the logits of the tile's rows (index positions, no early rows)
-      const int l = seg / p.Hkv, g = seg - l * p.Hkv;
+      const int sl = seg / p.Hkv, g = seg - sl * p.Hkv, l = p.l0 + sl;
       float *lg = p.logits + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * p.cap + (int64_t)tis * kTile;
       const bool c0 = kTwoN ? n0 < G : part0 == 0, c1 = kTwoN ? n0 + 1 < G : part1 == 0;
       const int h0 = kTwoN ? n0 : n0 % G, h1 = kTwoN ? n0 + 1 : (n0 + 1) % G;
@@ -1143,13 +1152,21 @@ extern "C" size_t zoomr_attn_workspace_bytes(const zoomr_geom *geom, int32_t bat
 static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
                               const int32_t *index, const int32_t *index_phys, const int32_t *index_count,
                               int32_t index_capacity, const int32_t *seq_len, int32_t sink, int32_t window,
-                              float softmax_scale, float *out, float *lse, void *workspace, size_t workspace_bytes,
-                              int32_t *dev_status, void *stream, float *logits = nullptr, bool chained = false) {
+                              float softmax_scale, int32_t layer_begin, int32_t layer_count, float *out, float *lse,
+                              void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream,
+                              float *logits = nullptr, bool chained = false) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !q || !kv || !kv->k || !kv->v || !kv->page_table || !index || !index_count ||
       index_capacity < 1 || !out || !workspace || kv->num_pages < 1 || kv->max_pages < 1)
     return ZOOMR_ERR_INVALID_ARG;
+  if (layer_count == 0) layer_count = geom->num_layers - layer_begin;  // 0: every layer from layer_begin on
+  if (layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > geom->num_layers) return ZOOMR_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  // Right behind a chained a5 on the same workspace (on this stream), the early
+  // rows would write the workspace while that launch may still be merging from
+  // it: attend index-only (nothing written before the wait) instead.
+  if (seq_len && prev_launch_is(s, kLaunchA5Chained, workspace)) seq_len = nullptr;
   if (batch > 65536) return ZOOMR_ERR_UNSUPPORTED;
   if (seq_len && (sink < 0 || window < 0)) return ZOOMR_ERR_INVALID_ARG;
   const size_t need = zoomr_attn_workspace_bytes(geom, batch);
@@ -1174,6 +1191,8 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   prm.ws_cnt = (int32_t *)((char *)workspace + ((part + 255) / 256) * 256);
   prm.B = batch;
   prm.L = geom->num_layers;
+  prm.l0 = layer_begin;
+  prm.Lc = layer_count;
   prm.Hkv = geom->num_kv_heads;
   prm.P = geom->page_size;
   // the page table is staged in shared memory before the wait, except in the
@@ -1190,7 +1209,6 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   prm.window = window;
   prm.status = dev_status;
   const int G = geom->num_q_heads / geom->num_kv_heads;
-  cudaStream_t s = (cudaStream_t)stream;
   const int grid = attn_grid(seq_len != nullptr);
   TmaMaps maps;
   {
@@ -1227,38 +1245,42 @@ static int sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void 
   }
 #undef ZOOMR_AT_G
 #undef ZOOMR_AT
-  return launch_status();
+  return launch_status(s, chained ? kLaunchA5Chained : kLaunchOther, workspace);
 }
 
 extern "C" int zoomr_sparse_decode_attn(const zoomr_geom *geom, int32_t batch, const void *q,
                                         const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                         const int32_t *index_count, int32_t index_capacity,
                                         const int32_t *seq_len, int32_t sink, int32_t window,
-                                        float softmax_scale, float *out, void *workspace,
-                                        size_t workspace_bytes, int32_t *dev_status, void *stream) {
+                                        float softmax_scale, int32_t layer_begin, int32_t layer_count, float *out,
+                                        void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream) {
   return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
-                            softmax_scale, out, nullptr, workspace, workspace_bytes, dev_status, stream);
+                            softmax_scale, layer_begin, layer_count, out, nullptr, workspace, workspace_bytes,
+                            dev_status, stream);
 }
 
 extern "C" int zoomr_sparse_decode_attn_chained(const zoomr_geom *geom, int32_t batch, const void *q,
                                                 const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                                 const int32_t *index_count, int32_t index_capacity,
                                                 const int32_t *seq_len, int32_t sink, int32_t window,
-                                                float softmax_scale, float *out, void *workspace,
-                                                size_t workspace_bytes, int32_t *dev_status, void *stream) {
+                                                float softmax_scale, int32_t layer_begin, int32_t layer_count,
+                                                float *out, void *workspace, size_t workspace_bytes,
+                                                int32_t *dev_status, void *stream) {
   return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
-                            softmax_scale, out, nullptr, workspace, workspace_bytes, dev_status, stream, nullptr,
-                            true);
+                            softmax_scale, layer_begin, layer_count, out, nullptr, workspace, workspace_bytes,
+                            dev_status, stream, nullptr, true);
 }
 
 extern "C" int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
                                             const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
                                             const int32_t *index_count, int32_t index_capacity, float softmax_scale,
-                                            float *out, float *lse, void *workspace, size_t workspace_bytes,
-                                            int32_t *dev_status, void *stream) {
+                                            int32_t layer_begin, int32_t layer_count, float *out, float *lse,
+                                            void *workspace, size_t workspace_bytes, int32_t *dev_status,
+                                            void *stream) {
   if (!lse) return ZOOMR_ERR_INVALID_ARG;
   return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, nullptr, 0, 0,
-                            softmax_scale, out, lse, workspace, workspace_bytes, dev_status, stream);
+                            softmax_scale, layer_begin, layer_count, out, lse, workspace, workspace_bytes, dev_status,
+                            stream);
 }
 
 extern "C" int zoomr_sparse_decode_attn_logits(const zoomr_geom *geom, int32_t batch, const void *q,
@@ -1268,7 +1290,34 @@ extern "C" int zoomr_sparse_decode_attn_logits(const zoomr_geom *geom, int32_t b
                                                int32_t *dev_status, void *stream) {
   if (!lse || !logits) return ZOOMR_ERR_INVALID_ARG;
   return sparse_decode_attn(geom, batch, q, kv, index, nullptr, index_count, index_capacity, nullptr, 0, 0,
-                            softmax_scale, out, lse, workspace, workspace_bytes, dev_status, stream, logits);
+                            softmax_scale, 0, 0, out, lse, workspace, workspace_bytes, dev_status, stream, logits);
+}
+
+// ---- the per-stream record of the library's last launch (common.cuh) ----------
+namespace {
+struct LaunchRec {
+  int kind;
+  const void *ws;
+};
+std::mutex g_launch_mu;
+std::unordered_map<cudaStream_t, LaunchRec> g_launch;
+}  // namespace
+
+void zoomr::note_launch(cudaStream_t s, int kind, const void *ws) {
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  if (kind == kLaunchOther) {
+    auto it = g_launch.find(s);
+    if (it != g_launch.end()) g_launch.erase(it);  // the common case keeps the table empty
+  } else {
+    g_launch[s] = LaunchRec{kind, ws};
+  }
+}
+
+bool zoomr::prev_launch_is(cudaStream_t s, int kind, const void *ws) {
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  auto it = g_launch.find(s);
+  if (it == g_launch.end()) return kind == kLaunchOther;
+  return it->second.kind == kind && (!ws || it->second.ws == ws);
 }
 
 extern "C" const char *zoomr_status_str(int status) {

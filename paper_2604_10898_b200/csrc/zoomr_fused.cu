@@ -61,7 +61,7 @@ struct FusedParams {
   int32_t *status;
   int32_t stop_after;  // debug A/B only: 0 full; 1 after the ticket; 2 after collect; 3 after a3
   int32_t pdl_front;  // chained: launched with PDL after a5; a1/a2 run before griddepcontrol.wait, a3/a4 after
-  int32_t designated_tail;  // the grid is resident at once: the last-launched CTA of b runs a3/a4
+  int32_t designated_tail;  // cooperative launch (grid co-resident): the last-launched CTA of b runs a3/a4
   const uint8_t *update;    // nullable: update[b] == 0 keeps b's flags (no a2/a3; a1 and a4 still run)
 };
 
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   // The CTA launched last for sequence b carries on: the others count
   // themselves with a fire-and-forget release add and exit at once (their SMs
   // go to a5 a round trip earlier); it waits (acquire) until all have counted.
-  // Used only when the whole grid is resident at once (host check), so the
-  // CTAs it waits for are running.
+  // Used only under a cooperative launch (the whole grid is resident at once),
+  // so the CTAs it waits for are running.
   const int nlg = p.L * p.Hkv;
   if (lg != nlg - 1) {
     if (threadIdx.x == 0)
@@ -323,14 +323,20 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   p.Hkv = geom->num_kv_heads;
   p.P = geom->page_size;
   p.status = dev_status;
-  p.pdl_front = chained ? 1 : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  // The chained variant overlaps a1/a2 with its predecessor only when that
+  // predecessor is the library's chained a5 (which writes none of a1/a2's
+  // inputs); after anything else it is launched like the plain one.
+  p.pdl_front = chained && prev_launch_is(s, kLaunchA5Chained, nullptr) ? 1 : 0;
+  p.stop_after = 0;
+#ifdef ZOOMR_EXPERIMENTS
   {
-    const char *e = getenv("ZOOMR_FUSED_STOP");
+    const char *e = getenv("ZOOMR_FUSED_STOP");  // experiment builds only: cut the kernel short for A/B timing
     p.stop_after = e ? atoi(e) : 0;
   }
+#endif
   const int G = geom->num_q_heads / geom->num_kv_heads;
   dim3 grid(geom->num_layers * geom->num_kv_heads, batch);
-  cudaStream_t s = (cudaStream_t)stream;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
     auto kfn = fused_select_kernel<DD, GG>;                                                      \
@@ -340,8 +346,12 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
     prefer_max_smem(kfn);                                                                        \
     int per_sm = 0;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);                      \
-    p.designated_tail = (int64_t)grid.x * grid.y <= (int64_t)per_sm * num_sms();                \
-    if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                            \
+    /* the designated tail spins on its siblings: only under a cooperative launch, which      \
+       guarantees that the whole grid is resident at once (never in the chained variant,      \
+       whose CTAs may wait for SMs still held by the preceding a5) */                          \
+    p.designated_tail = !p.pdl_front && (int64_t)grid.x * grid.y <= (int64_t)per_sm * num_sms(); \
+    if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                                     \
+    else if (p.designated_tail) launch_cooperative(kfn, grid, 256, smem, s, p);                  \
     else kfn<<<grid, 256, smem, s>>>(p);                                                         \
   } while (0)
 #define ZOOMR_FS_G(DD)               \
@@ -360,7 +370,7 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   }
 #undef ZOOMR_FS_G
 #undef ZOOMR_FS
-  return launch_status();
+  return launch_status(s);
 }
 
 #define ZOOMR_SELECT_FUSED_ARGS                                                                                 \

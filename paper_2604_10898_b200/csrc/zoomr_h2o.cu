@@ -260,7 +260,7 @@ extern "C" int zoomr_h2o_accumulate(const zoomr_geom *geom, int32_t batch, const
   h2o_accumulate_kernel<<<grid, kAccTok * kAccGrp, 0, (cudaStream_t)stream>>>(
       index, index_count, index_capacity, geom->num_layers * geom->num_q_heads, logits, lse, score, score_stride,
       index_copy, count_copy, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }
 
 extern "C" int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *prev_count,
@@ -275,5 +275,5 @@ extern "C" int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const 
   h2o_select_kernel<<<batch, kSelThreads, smem, (cudaStream_t)stream>>>(prev_index, prev_count, index_capacity,
                                                                        score, score_stride, seq_len, sink, window,
                                                                        budget, index, index_count, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

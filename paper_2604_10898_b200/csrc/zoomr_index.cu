@@ -60,5 +60,5 @@ extern "C" int zoomr_build_index(int32_t batch, const zoomr_segments *seg, const
   build_index_kernel<<<batch, 512, smem, (cudaStream_t)stream>>>(
       seg->bounds, seg->num_summaries, seg->seq_len, seg->max_summaries, flags, sink, window,
       index, index_capacity, index_count, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -104,7 +104,7 @@ extern "C" int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoom
       kv->page_table, kv->max_pages, geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, seq_len,
       0, dev_status);
   advance_kernel<<<(batch + 127) / 128, 128, 0, s>>>(seq_len, batch);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }
 
 extern "C" int zoomr_write_newest_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
@@ -118,7 +118,7 @@ extern "C" int zoomr_write_newest_kv(const zoomr_geom *geom, int32_t batch, cons
       (const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k, (__nv_bfloat16 *)kv->v, kv->num_pages,
       kv->page_table, kv->max_pages, geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, seq_len,
       1, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }
 
 extern "C" int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
@@ -131,5 +131,5 @@ extern "C" int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int
   track_kernel<<<(batch + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
       batch, token_ids, begin_id, end_id, boundary_ids, n_boundary, seq_len, bounds, num_summaries, max_summaries,
       reinterpret_cast<int4 *>(state), close_items, update, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -73,5 +73,5 @@ extern "C" int zoomr_update_mean_keys(const zoomr_geom *geom, int32_t batch, con
     default: ZOOMR_MK(128); break;
   }
 #undef ZOOMR_MK
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -110,5 +110,5 @@ extern "C" int zoomr_score(const zoomr_geom *geom, int32_t batch, const void *q,
   }
 #undef ZOOMR_SC_G
 #undef ZOOMR_SC
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -58,5 +58,5 @@ extern "C" int zoomr_select_topc(int32_t batch, const int64_t *partial,
   prefer_max_smem(select_topc_kernel);
   select_topc_kernel<<<batch, 512, smem, (cudaStream_t)stream>>>(partial, num_summaries, max_summaries, c,
                                                                  flags, agreeability, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -149,7 +149,7 @@ extern "C" int zoomr_shard_index(int32_t batch, const int32_t *index, const int3
     return ZOOMR_ERR_INVALID_ARG;
   launch_pdl(shard_index_kernel, batch, kShardThreads, 0, (cudaStream_t)stream, index, index_count, index_capacity,
              owner, owner_stride, rank, local_index, local_count, dev_status);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }
 
 extern "C" int zoomr_merge_attn(const zoomr_geom *geom, int32_t batch, int32_t n_parts, const float *part_out,
@@ -165,5 +165,5 @@ extern "C" int zoomr_merge_attn(const zoomr_geom *geom, int32_t batch, int32_t n
   if (grid > 0x7fffffff) return ZOOMR_ERR_UNSUPPORTED;
   merge_attn_kernel<<<(unsigned)grid, 32 * wpb, 0, (cudaStream_t)stream>>>(
       rows, rps, batch, geom->head_dim, n_parts, part_out, part_lse, part_count, out, lse);
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -270,10 +270,10 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
   tier_plan_kernel<<<1, kPlanThreads, 0, s>>>(batch, index, index_count, index_capacity, Ph, R, host_kv->max_pages,
                                               host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
                                               (int32_t *)workspace, dev_status);
-  rc = launch_status();
+  rc = launch_status(s);
   if (rc) return rc;
   launch_pdl(tier_copy_kernel, 2 * num_sms(), 256, 0, s, (const uint4 *)host_kv->k, (const uint4 *)host_kv->v,
              (int64_t)host_kv->num_pages, (uint4 *)hot_k, (uint4 *)hot_v, (int64_t)hot_pages, geom->num_layers,
              geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp));
-  return launch_status();
+  return launch_status((cudaStream_t)stream);
 }

@@ -33,8 +33,10 @@ class ZoomrStep:
         self.shape, self.batch, self.params = shape, batch, params
         # steps enqueued back to back (several per CUDA graph): the fused select of
         # step t+1 runs a1/a2 while a5 of step t finishes (zoomr_*_chained)
+        # (libzoomr checks the launch order itself: after anything but a chained a5 the
+        # chained select runs like the plain one, and an a5 right behind a chained a5 on
+        # the same workspace attends index-only -- zoomr.h "Chained launches")
         self.chained = chained
-        self._chained_a5_last = False  # this step's last launch was a chained a5 (see attend)
         self.max_summaries, self.cap = max_summaries, index_capacity
         dev = torch.device(device)
         L, Hq, Hkv, d = shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
@@ -63,7 +65,6 @@ class ZoomrStep:
     def update_mean_keys(self, kv, seg, items: torch.Tensor):
         k_pool, v_pool, page_table = kv
         bounds, nsum, seq_len = seg
-        self._chained_a5_last = False
         Z.update_mean_keys(self.shape, k_pool, v_pool, page_table, bounds, nsum, seq_len, items,
                            self.mean_keys, self.status)
 
@@ -88,7 +89,6 @@ class ZoomrStep:
         k_pool, v_pool, page_table = kv
         bounds, nsum, seq_len = seg
         p = self.params
-        self._chained_a5_last = False  # a select / index launch comes first
         if fused and update_selection and allreduce is None:
             # a1..a4 in one launch (zoomr_select_fused), then a5
             Z.select_fused(self.shape, q, k_pool, v_pool, page_table, bounds, nsum, seq_len,
@@ -119,16 +119,11 @@ class ZoomrStep:
         k_pool, v_pool, page_table = kv
         use_phys = self.use_phys if phys is None else phys
         p = self.params
-        # right behind a chained a5 on the same workspace (zoomr.h's contract), the
-        # early rows would write the workspace while that launch still merges:
-        # attend index-only instead (nothing is written before the wait)
-        early = self.early_known and not self._chained_a5_last
         Z.sparse_decode_attn(self.shape, q, k_pool, v_pool, page_table, self.index, self.count,
                              self.out, self.workspace, dev_status=self.status,
                              index_phys=self.index_phys if use_phys else None,
-                             seq_len=seq_len if early else None, sink=p.sink, window=p.window,
+                             seq_len=seq_len if self.early_known else None, sink=p.sink, window=p.window,
                              chained=chained)
-        self._chained_a5_last = chained
 
     def launches_per_step(self, update_selection=True, close=False, fused=True) -> int:
         """Kernel launches one run() enqueues (a2 = zero + score when not fused)."""
@@ -209,7 +204,6 @@ class DecodeLoop(ZoomrStep):
         """Enqueue one step; k_new/v_new bf16 [B][L][H_kv][d], q bf16 [B][L][H_q][d], token_ids int32 [B]."""
         k_pool, v_pool, page_table = kv
         p = self.params
-        self._chained_a5_last = False
         Z.append_kv(self.shape, k_pool, v_pool, page_table, k_new, v_new, self.seq_len, self.status)
         Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
                          self.num_summaries, self.track_state, self.close_items, self.update, self.status)

@@ -51,7 +51,7 @@ class Segments(C.Structure):
                 ("max_summaries", C.c_int32)]
 
 
-ABI_VERSION = 8  # include/zoomr.h ZOOMR_ABI_VERSION
+ABI_VERSION = 9  # include/zoomr.h ZOOMR_ABI_VERSION
 _lib = None
 
 
@@ -70,8 +70,9 @@ def lib():
         L.zoomr_build_index.argtypes = [i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]
         L.zoomr_attn_workspace_bytes.argtypes = [vp, i32]
         L.zoomr_attn_workspace_bytes.restype = sz
-        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, vp, vp, sz,
-                                               vp, vp]
+        L.zoomr_sparse_decode_attn.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, i32, i32,
+                                               vp, vp, sz, vp, vp]
+        L.zoomr_sparse_decode_attn_chained.argtypes = L.zoomr_sparse_decode_attn.argtypes
         L.zoomr_select_workspace_bytes.argtypes = [vp, i32, i32]
         L.zoomr_select_workspace_bytes.restype = sz
         L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp,
@@ -83,8 +84,8 @@ def lib():
         L.zoomr_track_segments.restype = C.c_int
         L.zoomr_shard_index.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp]
         L.zoomr_shard_index.restype = C.c_int
-        L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, vp, vp, vp, sz,
-                                                   vp, vp]
+        L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, i32, i32, vp, vp, vp,
+                                                   sz, vp, vp]
         L.zoomr_sparse_decode_attn_lse.restype = C.c_int
         L.zoomr_merge_attn.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_merge_attn.restype = C.c_int
@@ -105,7 +106,7 @@ def lib():
         L.zoomr_status_str.restype = C.c_char_p
         L.zoomr_abi_version.restype = C.c_int
         for fn in (L.zoomr_update_mean_keys, L.zoomr_score, L.zoomr_select_topc,
-                   L.zoomr_build_index, L.zoomr_sparse_decode_attn):
+                   L.zoomr_build_index, L.zoomr_sparse_decode_attn, L.zoomr_sparse_decode_attn_chained):
             fn.restype = C.c_int
         if L.zoomr_abi_version() != ABI_VERSION:
             raise ImportError(f"{LIB_PATH} has ABI {L.zoomr_abi_version()}, this binding expects {ABI_VERSION}: "
@@ -230,10 +231,11 @@ def attn_workspace_bytes(shape: Shape, batch: int) -> int:
 
 def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out,
                        workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
-                       seq_len=None, sink=0, window=0, chained=False):
+                       seq_len=None, sink=0, window=0, chained=False, layer_begin=0, layer_count=0):
     """a5 (zoomr_sparse_decode_attn). workspace: uint8 CUDA tensor, zeroed once.
     chained: zoomr_sparse_decode_attn_chained (a PDL-launched successor, normally
     select_fused(chained=True) of the next step, may start during this launch).
+    layer_begin/layer_count: attend only those layers (0 = through the last).
 
     seq_len/sink/window (optional): `index` is a4's output for these values, so
     I_p and I_w are attended before the kernel waits for I_f (see zoomr.h)."""
@@ -245,7 +247,8 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
                                         _ptr(index_phys, torch.int32, "index_phys"),
                                         _ptr(index_count, torch.int32, "index_count"), index.shape[1],
                                         _ptr(seq_len, torch.int32, "seq_len"), int(sink), int(window),
-                                        C.c_float(sc), _ptr(out, torch.float32, "out"),
+                                        C.c_float(sc), int(layer_begin), int(layer_count),
+                                        _ptr(out, torch.float32, "out"),
                                         _ptr(workspace, None, "workspace"), workspace.numel() *
                                         workspace.element_size(),
                                         _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
@@ -253,7 +256,8 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
 
 
 def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out, lse,
-                           workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None):
+                           workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
+                           layer_begin=0, layer_count=0):
     """a5 over any index list, also writing lse fp32 [B][L][H_q] (zoomr_sparse_decode_attn_lse)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
@@ -261,7 +265,8 @@ def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, i
                                             C.byref(kv), _ptr(index, torch.int32, "index"),
                                             _ptr(index_phys, torch.int32, "index_phys"),
                                             _ptr(index_count, torch.int32, "index_count"), index.shape[1],
-                                            C.c_float(sc), _ptr(out, torch.float32, "out"),
+                                            C.c_float(sc), int(layer_begin), int(layer_count),
+                                            _ptr(out, torch.float32, "out"),
                                             _ptr(lse, torch.float32, "lse"), _ptr(workspace, None, "workspace"),
                                             workspace.numel() * workspace.element_size(),
                                             _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))

@@ -46,7 +46,7 @@ def test_status_strings_and_version(lib):
     assert lib.zoomr_status_str(0) == b"ZOOMR_OK"
     assert lib.zoomr_status_str(6) == b"ZOOMR_ERR_CAPACITY"
     assert lib.zoomr_status_str(999) == b"ZOOMR_ERR_UNKNOWN"
-    assert lib.zoomr_abi_version() == 8
+    assert lib.zoomr_abi_version() == 9
 
 
 def test_host_argument_errors_without_a_device(lib):

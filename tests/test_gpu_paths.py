@@ -221,3 +221,145 @@ def test_chained_steps_in_one_graph(cfg):
     st.check_status()
     assert (st.out - ref.out).abs().max().item() <= 1e-5
     assert "zoomr_select_fused_chained" in Z.EXPORTS
+
+
+@pytest.mark.parametrize("cfg", [
+    _small("chain1_b3", d=128, batch=3),
+    dataclasses.replace(S.stress_config(64, 8), name="chain1_stress_LR64", seed=13),
+    dataclasses.replace(S.CONFIGS["8b16k"], seed=14, batch=2),
+], ids=lambda c: c.name)
+def test_chained_same_object_back_to_back(cfg):
+    """ONE ZoomrStep(chained=True) run N times back to back inside one graph (the
+    serving-loop case: every select and a5 share one selection workspace and one
+    attention workspace), the queries alternating between two sets so that
+    consecutive steps select different summaries.  Each select(t+1) may start
+    only after select(t) completed (a5(t) triggers after its wait): a vote or
+    ticket of step t+1 landing while step t still aggregates would leave the
+    self-resetting workspaces dirty and the outputs wrong.  Checked: the last
+    step's outputs equal the same step run alone (unchained), and both
+    workspaces are all-zero after every replay -- at the configs[4] point with
+    the longest select tail (L_R = 64, N_t = 1631) and at batch > 1."""
+    inp = S.generate(cfg, device="cuda")
+    cap = 40000 if cfg.T > 4096 else None
+    g2 = torch.Generator(device="cuda").manual_seed(cfg.seed + 99)
+    q_b = (0.25 * torch.randn(inp.q.shape, device="cuda", generator=g2)).bfloat16()  # diffuse: other summaries
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    newest = torch.tensor([[b, int(n) - 1] for b, n in enumerate(inp.num_summaries.cpu().tolist())],
+                          dtype=torch.int32, device="cuda")
+    refs = {}
+    for name, q in (("a", inp.q), ("b", q_b)):
+        ref = PY.make_step(inp, debug=False, capacity=cap)
+        ref.update_mean_keys(kv, seg, ref.all_items(inp.num_summaries))
+        ref.run(q, kv, seg, close_items=newest)
+        torch.cuda.synchronize()
+        ref.check_status()
+        refs[name] = ref
+    st = PY.make_step(inp, debug=False, capacity=cap)
+    st.chained = True
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        st.run(inp.q, kv, seg, close_items=newest)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    N = 8
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(N):
+            st.run(inp.q if i % 2 == 0 else q_b, kv, seg, close_items=newest)
+    last = refs["b"]  # N even: the last step used q_b
+    for _ in range(4):
+        st.out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        st.check_status()
+        assert torch.equal(st.count, last.count)
+        for b in range(inp.q.shape[0]):
+            n = int(st.count[b])
+            assert torch.equal(st.index[b, :n], last.index[b, :n])
+        assert torch.equal(st.flags, last.flags)
+        assert torch.equal(st.partial, last.partial)
+        assert torch.equal(st.out, last.out)
+        assert int(st.sel_workspace.count_nonzero()) == 0, "selection workspace left dirty"
+        ws_cnt_bytes = inp.q.shape[0] * cfg.L * cfg.Hkv * 4
+        assert int(st.workspace[-ws_cnt_bytes:].count_nonzero()) == 0, "a5 arrival counters left dirty"
+
+
+def test_a5_behind_chained_a5_same_workspace():
+    """The old caller rule (zoomr.h ABI 8: "the kernel following a chained a5 must
+    not be a PDL-launched a5 using the same workspace") deliberately broken: a
+    chained a5 followed directly by an a5 WITH the early rows (which write the
+    workspace before their wait), on one workspace, alternating queries, 10
+    times in one graph.  The library detects the order and runs the second a5
+    index-only; every output equals the a5 run alone."""
+    from paper_2604_10898_b200 import zoomr as Z
+    cfg = dataclasses.replace(S.CONFIGS["8b16k"], seed=15)
+    inp = S.generate(cfg, device="cuda")
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    st = PY.make_step(inp, debug=False, capacity=8192)
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    st.run(inp.q, kv, seg)
+    g2 = torch.Generator(device="cuda").manual_seed(7)
+    q_b = (0.25 * torch.randn(inp.q.shape, device="cuda", generator=g2)).bfloat16()
+    outs = {}
+    for name, q in (("a", inp.q), ("b", q_b)):
+        o = torch.zeros_like(st.out)
+        Z.sparse_decode_attn(st.shape, q, *kv, st.index, st.count, o, st.workspace, dev_status=st.status)
+        outs[name] = o
+    torch.cuda.synchronize()
+    oa, ob = torch.zeros_like(st.out), torch.zeros_like(st.out)
+    args = dict(dev_status=st.status)
+    Z.sparse_decode_attn(st.shape, inp.q, *kv, st.index, st.count, oa, st.workspace, chained=True, **args)
+    Z.sparse_decode_attn(st.shape, q_b, *kv, st.index, st.count, ob, st.workspace, seq_len=inp.seq_len,
+                         sink=cfg.sink, window=cfg.window, **args)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(10):
+            Z.sparse_decode_attn(st.shape, inp.q, *kv, st.index, st.count, oa, st.workspace, chained=True, **args)
+            Z.sparse_decode_attn(st.shape, q_b, *kv, st.index, st.count, ob, st.workspace, seq_len=inp.seq_len,
+                                 sink=cfg.sink, window=cfg.window, **args)
+    for _ in range(3):
+        oa.zero_()
+        ob.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        st.check_status()
+        assert torch.equal(oa, outs["a"])
+        assert torch.equal(ob, outs["b"])
+
+
+@pytest.mark.parametrize("ranges", [[(0, 1), (1, 0)], [(0, 3), (3, 2), (5, 3)]], ids=["2_ranges", "3_ranges"])
+def test_a5_layer_ranges(ranges):
+    """a5 with layer_begin / layer_count: attending the layers in
+    pieces gives the output of one all-layer launch (to fp32 rounding: the
+    stream-K split, hence the summation order, depends on the launch's work),
+    and a launch leaves the out rows of the other layers untouched."""
+    from paper_2604_10898_b200 import zoomr as Z
+    cfg = _small("layers", L=8, d=128, batch=2, Hq=8, Hkv=2)
+    inp = S.generate(cfg, device="cuda")
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    st = PY.make_step(inp, debug=False)
+    PY.run_full(inp, st, fused=True)
+    full = st.out.clone()
+    out = torch.full_like(full, 7.0)
+    for lb, lc in ranges:
+        Z.sparse_decode_attn(st.shape, inp.q, *kv, st.index, st.count, out, st.workspace, dev_status=st.status,
+                             layer_begin=lb, layer_count=lc)
+        torch.cuda.synchronize()
+        hi = cfg.L if lc == 0 else lb + lc
+        assert (out[:, lb:hi] - full[:, lb:hi]).abs().max().item() <= 1e-5
+        assert bool((out[:, hi:] == 7.0).all())
+    lse = torch.zeros(inp.q.shape[0], cfg.L, cfg.Hq, device="cuda")
+    o2 = torch.zeros_like(full)
+    Z.sparse_decode_attn_lse(st.shape, inp.q, *kv, st.index, st.count, o2, lse, st.workspace, layer_begin=2,
+                             layer_count=3)
+    torch.cuda.synchronize()
+    assert (o2[:, 2:5] - full[:, 2:5]).abs().max().item() <= 1e-5
+    assert bool((lse[:, :2] == 0).all()) and bool((lse[:, 5:] == 0).all()) and bool((lse[:, 2:5] != 0).all())
+    with pytest.raises(Z.ZoomrError):
+        Z.sparse_decode_attn(st.shape, inp.q, *kv, st.index, st.count, out, st.workspace, layer_begin=7,
+                             layer_count=2)

@@ -832,7 +832,8 @@ def run_ours(args):
                 lp.decode_step(s0["kv"], kin, vin, inp0.q, tok_dev[i])
 
         def loop_run():
-            lp.seq_len.copy_(start)
+            lp.start_from(bpad, inp0.num_summaries, start)  # T, N_t, segment table, tracker: as at the start
+            lp.flags[:, :nmax0].copy_(s0["st"].flags)  # the selection made before the stretch (held until a boundary)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

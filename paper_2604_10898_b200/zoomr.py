@@ -437,3 +437,31 @@ def track_segments(token_ids, begin_id, end_id, boundary_ids, seq_len, bounds, n
         _ptr(state, torch.int32, "state"), _ptr(close_items, torch.int32, "close_items"),
         _ptr(update, torch.uint8, "update"), _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_track_segments", rc)
+
+
+# ---- NVTX: one range per enqueued stage (host-side marks; visible to ncu --nvtx / nsys) ----------
+_STAGES = {
+    "update_mean_keys": "a1", "score": "a2", "select_topc": "a3", "build_index": "a4",
+    "sparse_decode_attn": "a5", "select_fused": "a1-a4", "append_kv": "a0", "track_segments": "a0",
+    "shard_index": "a4-shard", "sparse_decode_attn_lse": "a5-lse", "merge_attn": "a5-merge",
+    "sparse_decode_attn_logits": "a5-logits", "h2o_accumulate": "h2o", "h2o_select": "h2o",
+    "tier_fetch": "tier", "write_newest_kv": "a0-tier",
+}
+
+
+def _nvtx_wrap(fn, label):
+    import functools
+
+    @functools.wraps(fn)
+    def w(*a, **k):
+        torch.cuda.nvtx.range_push(label)
+        try:
+            return fn(*a, **k)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    return w
+
+
+if os.environ.get("ZOOMR_NVTX", "1") != "0":
+    for _n, _s in _STAGES.items():
+        globals()[_n] = _nvtx_wrap(globals()[_n], f"{_s} zoomr_{_n}")

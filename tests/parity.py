@@ -112,8 +112,10 @@ def check_sequence(inp, step, b, report):
         assert np.all(np.abs(A_gpu - A_ref) <= ALPHA_TOL * np.maximum(Mv, 1e-30) + 2.0 ** -32 * L * Hq)
         # a3: flags from the GPU's (v, A) are bit-exact (integer keys, same total order)
         flags_gpu = step.flags[b, :n].cpu().numpy()
-        flags_same_in, _, _ = oracle.select_topc(part[0], A_gpu, cfg.c)
+        flags_same_in, ag_same_in, _ = oracle.select_topc(part[0], A_gpu, cfg.c)
         assert np.array_equal(flags_gpu, flags_same_in), "a3 flags differ on identical (v, A)"
+        # AG: the kernel's fp64 ratio of integer vote sums, rounded once to fp32
+        check_ag(step, b, ag_same_in, report)
         # ... and equal to the oracle's flags from its own A, modulo a certified cut near-tie
         flags_ref, _, cut_near = oracle.select_topc(votes_ref, A_ref, cfg.c)
         if not np.array_equal(flags_gpu, flags_ref):
@@ -136,6 +138,13 @@ def check_sequence(inp, step, b, report):
     assert e <= ATTN_TOL, f"attention max abs err {e}"
     # planted-relevance recall (S:483 style, informational)
     return report
+
+
+def check_ag(step, b, ag_ref, report):
+    """GPU agreeability == the oracle's AG on the same (v, A), rounded to fp32 (bit-exact)."""
+    ag_gpu = float(step.agreeability[b].item())
+    assert ag_gpu == float(np.float32(ag_ref)), f"AG {ag_gpu} vs oracle {ag_ref}"
+    report.setdefault("agreeability", []).append(ag_gpu)
 
 
 def cfg_sink(step):
@@ -195,16 +204,19 @@ def gather_tokens(inp, b, positions, which="k", layers=None, heads=None):
     slots = pos % cfg.page
     lay = torch.arange(cfg.L, device=dev) if layers is None else torch.as_tensor(list(layers), device=dev)
     hed = torch.arange(cfg.Hkv, device=dev) if heads is None else torch.as_tensor(list(heads), device=dev)
-    sub = pool.index_select(0, lay)                      # [L'][pages][Hkv][P][d]
+    sub = pool if layers is None else pool.index_select(0, lay)  # [L'][pages][Hkv][P][d]
     rows = sub[:, pages, :, slots]     # advanced indices separated by a slice go first: [n][L'][Hkv][d]
-    rows = rows.index_select(2, hed)   # [n][L'][H'][d]
+    if heads is not None:
+        rows = rows.index_select(2, hed)   # [n][L'][H'][d]
     return bf16_bits(rows.contiguous())
 
 
-def check_sequence_sampled(inp, step, b, report, layers, qheads):
-    """Full-size parity on sampled outputs: selection over ALL voters (votes are a
-    global aggregate), mean keys / alpha checked on every layer, attention on the
-    sampled (layer, query head) pairs only."""
+def check_sequence_sampled(inp, step, b, report, layers=None, qheads=None):
+    """Full-size parity: selection over ALL voters (votes are a global aggregate),
+    mean keys / alpha checked on every layer; attention on the given (layer,
+    query head) pairs, or -- layers=None -- on EVERY (layer, head) output (the
+    rows of I_f are gathered once for all layers and heads and the OpenMP
+    oracle attends over them)."""
     cfg = inp.cfg
     L, Hq, Hkv, d = cfg.L, cfg.Hq, cfg.Hkv, cfg.d
     G = Hq // Hkv
@@ -242,8 +254,9 @@ def check_sequence_sampled(inp, step, b, report, layers, qheads):
     assert np.array_equal(part[0], votes_ref), "votes differ"
     A_gpu = part[1].astype(np.float64) / 2.0 ** 32
     flags_gpu = step.flags[b, :n].cpu().numpy()
-    flags_same_in, _, _ = oracle.select_topc(part[0], A_gpu, cfg.c)
+    flags_same_in, ag_same_in, _ = oracle.select_topc(part[0], A_gpu, cfg.c)
     assert np.array_equal(flags_gpu, flags_same_in)
+    check_ag(step, b, ag_same_in, report)
     flags_ref, _, _ = oracle.select_topc(votes_ref, A_ref, cfg.c)
     if not np.array_equal(flags_gpu, flags_ref):
         zc_g, zc_r = set(np.nonzero(flags_gpu == 2)[0]), set(np.nonzero(flags_ref == 2)[0])
@@ -254,6 +267,15 @@ def check_sequence_sampled(inp, step, b, report, layers, qheads):
     assert cnt == len(idx_ref) and np.array_equal(step.index[b, :cnt].cpu().numpy(), idx_ref)
     report.setdefault("index_counts", []).append(cnt)
     out_gpu = step.out[b].cpu().numpy().astype(np.float64)
+    if layers is None:
+        Kr = gather_tokens(inp, b, idx_ref, "k")  # [|I_f|][L][H_kv][d]
+        Vr = gather_tokens(inp, b, idx_ref, "v")
+        o = oracle.sparse_decode_attn(q, Kr, Vr, np.arange(len(idx_ref), dtype=np.int32), L, Hq, Hkv, d)
+        e = float(np.abs(out_gpu - o).max())
+        report["attn_max_abs_err"] = max(report.get("attn_max_abs_err", 0.0), e)
+        report["attn_outputs_checked"] = report.get("attn_outputs_checked", 0) + L * Hq
+        assert e <= ATTN_TOL
+        return report
     kvheads = sorted({h // G for h in qheads})
     for l in layers:
         Kr = gather_tokens(inp, b, idx_ref, "k", layers=[l], heads=kvheads)

@@ -277,6 +277,31 @@ int zoomr_select_fused_chained(const zoomr_geom *geom, int32_t batch, const void
                                int32_t *topk_out, void *workspace, size_t workspace_bytes,
                                int32_t *dev_status, void *stream);
 
+/* The fused select split around the KV-head-sharded exchange (SURVEY 8(e).2,
+ * ABI 9): the caller all-reduces `partial` (SUM over ranks) between the two.
+ *   zoomr_select_front = a1 + a2 of zoomr_select_fused (mean keys of close_items,
+ *     alpha, per-voter top-k) for the rank's local heads, with the
+ *     cross-head / cross-layer aggregation: writes partial int64 [B][2][max_summaries]
+ *     = (votes, fixed-point A; entries >= N_t zero) -- the same values as
+ *     zoomr_score.  Sequences with update[b] == 0 are skipped (partial row
+ *     untouched).  workspace as for zoomr_select_fused (the same buffer may serve both).
+ *   zoomr_select_tail = a3 + a4 from a given partial: flags,
+ *     agreeability (nullable), I_f, count; one CTA per sequence.  kv may be NULL
+ *     unless index_phys is given (it supplies the page table).  Launched so that a
+ *     following a5 with early rows overlaps it.
+ * front + all-reduce + tail is bit-identical to zoomr_score + all-reduce +
+ * zoomr_select_topc + zoomr_build_index (and, on one rank, to zoomr_select_fused). */
+int zoomr_select_front(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                       const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                       const uint8_t *update, float *mean_keys, int32_t top_k, int64_t *partial,
+                       float *alpha_out, int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                       int32_t *dev_status, void *stream);
+
+int zoomr_select_tail(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const zoomr_segments *seg,
+                      const int64_t *partial, const uint8_t *update, int32_t c, int32_t sink, int32_t window,
+                      uint8_t *flags, float *agreeability, int32_t *index, int32_t *index_phys,
+                      int32_t index_capacity, int32_t *index_count, int32_t *dev_status, void *stream);
+
 /* ---- Algorithm 1's per-token bookkeeping, on device ----------
  *
  * a0 -- KV append, Alg.1 @P:407 ("Append k_t and v_t to KV cache"): writes the

@@ -269,6 +269,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     TL_CTA(1);
   }
 
+  if (S::SWZ && threadIdx.x < 6) {  // the tensor maps' descriptors, fetched while the prologue runs
+    const CUtensorMap *m = &maps.k32 + threadIdx.x;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+  }
   if (threadIdx.x == 0) {
     for (int x = 0; x < kPairs * kStages; ++x) {
       mbar_init(&full[x], 33);  // producer lane 0's expect_tx arrive + one cp.async (noinc) arrive per lane
@@ -471,16 +475,34 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     constexpr int kAheadA = 4, kAheadB = 2;
     Addr q0{}, q1{}, q2{}, q3{}, q4{};  // tiles k .. k+4
     int64_t ntiles = nAk;
+    int64_t kfill = 0;  // first tile of the current pass: stage C is skipped below it (pipeline fill)
     // one loop, one call site per stage (the pipeline fill is its first kAheadA
-    // iterations): the kernel's code stays small enough for the instruction cache
-    for (int64_t k = -kAheadA; k < ntiles; ++k) {
-      if (!bres && k + kAheadA >= nAk) {  // first phase-B tile enters the pipeline
+    // iterations): the kernel's code stays small enough for the instruction cache.
+    // Phase A's tiles are all issued BEFORE griddepcontrol.wait: the address
+    // pipeline stops at the phase boundary, and only when every phase-A copy is
+    // in flight does the producer wait for I_f (the ring still holds up to
+    // kStages phase-A tiles for its math warp, which cover the refill of the
+    // pipeline for phase B).  Waiting as soon as the first phase-B tile entered
+    // the pipeline (kAheadA tiles early) stalled the phase-A stream for the
+    // whole select tail.
+    for (int64_t k = -kAheadA;; ++k) {
+#ifdef ZOOMR_AB_OLD_WAIT  // A/B builds only: wait as soon as the first phase-B tile enters the pipeline
+      if (!bres && k + kAheadA >= nAk) {
         resolve_b();
         ntiles = nAk + nBk;
       }
+#endif
+      if (!bres && k >= nAk) {  // every phase-A tile issued: wait for I_f, then refill for phase B
+        resolve_b();
+        ntiles = nAk + nBk;
+        if (k >= ntiles) break;
+        k = nAk - kAheadA;
+        kfill = nAk;
+      }
+      if (k >= ntiles) break;
       if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
-      if (k + kAheadB >= 0 && k + kAheadB < ntiles) stage_b(q2);
-      if (k < 0) {
+      if (k + kAheadB >= kfill && k + kAheadB < ntiles) stage_b(q2);
+      if (k < kfill) {
         q0 = q1;
         q1 = q2;
         q2 = q3;

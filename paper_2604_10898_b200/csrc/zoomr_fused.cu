@@ -63,7 +63,15 @@ struct FusedParams {
   int32_t pdl_front;  // chained: launched with PDL after a5; a1/a2 run before griddepcontrol.wait, a3/a4 after
   int32_t designated_tail;  // cooperative launch (grid co-resident): the last-launched CTA of b runs a3/a4
   const uint8_t *update;    // nullable: update[b] == 0 keeps b's flags (no a2/a3; a1 and a4 still run)
+  int32_t mode;             // kFull a1..a4 | kFront a1 + a2 -> partial | kTail partial -> a3 + a4
 };
+
+// The KV-head-sharded step splits the fused select around its all-reduce
+// (SURVEY 8(e).2): the front (every (l, g) CTA: a1, a2, top-k, vote atomics;
+// the last CTA of b writes the rank's partial) and the tail (one CTA per
+// sequence: a3 + a4 from the all-reduced partial) -- two launches instead of
+// the five separate ones, and a5's early rows still overlap the tail.
+enum FusedMode : int { kFull = 0, kFront = 1, kTail = 2 };
 
 template <int D, int G>
 __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams p) {
@@ -84,8 +92,41 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   const int32_t *bd = p.bounds + (int64_t)b * MS * 4;
   float *mk = p.mean_keys + (((int64_t)b * p.L + l) * p.Hkv + g) * (int64_t)MS * D;
 
+  const bool tail_only = p.mode == kTail;  // grid (1, B): straight to the collect of the given partial
+  const int nlg = p.L * p.Hkv;
+  // designated tail: CTA nlg of sequence b does no (l, g) work; it runs the tail's
+  // code once on dummy shared-memory data while the others score (so a3/a4 then
+  // run from a warm instruction cache instead of fetching each new block of code
+  // through an L2 that a5's gather keeps flushing), then waits for their count
+  const bool tail_cta = p.designated_tail && lg == nlg;
+#ifndef ZOOMR_AB_NO_WARM  // A/B builds only: the tail CTA without the warm-up pass
+  if (tail_cta) {
+    SmemCarve sm{smem_raw};
+    long long *A = sm.take<long long>(MS);
+    int *v = sm.take<int>(MS);
+    int *grp = sm.take<int>(2 * MS);
+    int *hist = sm.take<int>(kHistBins);
+    int *scratch = sm.take<int>(40);
+    int4 *bds = sm.take<int4>(MS);
+    sm.take<int>(p.max_pages);
+    uint8_t *fl = sm.take<uint8_t>(MS);
+    __shared__ float warm_ag;
+    __shared__ int warm_count;
+    for (int i = threadIdx.x; i < MS; i += blockDim.x) {
+      v[i] = 1 + (i & 3);
+      A[i] = (long long)(i * 7919 % 1000) << 20;
+      bds[i] = make_int4(8 * i + 4, 8 * i + 8, 8 * i + 8, 8 * i + 12);
+    }
+    __syncthreads();
+    block_topc(v, A, nt, p.c > 0 ? p.c : 1, fl, hist, grp, scratch, &warm_ag);
+    __syncthreads();
+    block_build_index(reinterpret_cast<const int32_t *>(bds), nt, 8 * nt + 16, fl, 4, 8,
+                      reinterpret_cast<int32_t *>(A), 2 * MS, &warm_count, grp, scratch, nullptr);
+    __syncthreads();
+  }
+#endif
   // ---- a1: mean keys of the summaries of b that closed this step -----------
-  {
+  if (!tail_only && !tail_cta) {
     double *red = reinterpret_cast<double *>(smem_raw);  // [nwarps][D]
     for (int it = 0; it < p.n_items; ++it) {
       if (p.items[2 * it] != b) continue;
@@ -108,7 +149,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
 
   // ---- a2: alpha + per-voter top-k (only at a selection update) ---------------------
   const bool upd = !p.update || p.update[b];
-  if (upd) {
+  if (upd && !tail_only && !tail_cta) {
     float *qs = reinterpret_cast<float *>(smem_raw);                 // [G][D]
     float *al = qs + G * D;                                          // [G][MS]
     int *sel_i = reinterpret_cast<int *>(al + G * MS);               // [G][k]
@@ -133,14 +174,13 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   // cumulative at gpu scope); the winner's acquire + bar.sync order its reads after.
   __syncthreads();
   if (threadIdx.x == 0) TL(1);
-  if (p.designated_tail) {
-  // The CTA launched last for sequence b carries on: the others count
-  // themselves with a fire-and-forget release add and exit at once (their SMs
-  // go to a5 a round trip earlier); it waits (acquire) until all have counted.
-  // Used only under a cooperative launch (the whole grid is resident at once),
-  // so the CTAs it waits for are running.
-  const int nlg = p.L * p.Hkv;
-  if (lg != nlg - 1) {
+  if (tail_only) {
+  } else if (p.designated_tail) {
+  // The (l, g) CTAs count themselves with a fire-and-forget release add and exit
+  // at once (their SMs go to a5 a round trip earlier); the tail CTA waits
+  // (acquire) until all have counted.  Used only under a cooperative launch
+  // (the whole grid is resident at once), so the CTAs it waits for are running.
+  if (!tail_cta) {
     if (threadIdx.x == 0)
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ws_ticket + b) : "memory");
     return;
@@ -149,7 +189,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ws_ticket + b) : "memory");
-    } while (v != (unsigned)(nlg - 1));
+    } while (v != (unsigned)nlg);
   }
   __syncthreads();
   } else {
@@ -166,7 +206,10 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
     allow_dependents();
   }
   if (threadIdx.x == 0) TL(2);
-  if (p.stop_after == 1) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
+  if (p.stop_after == 1 || (p.mode == kFront && !upd)) {  // (front without an update: only a1 had work)
+    if (threadIdx.x == 0) p.ws_ticket[b] = 0;
+    return;
+  }
 
   // ---- aggregation (a2, cross-head / cross-layer), exact integer atomics --------
   SmemCarve sm{smem_raw};
@@ -194,7 +237,10 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
       const int i = i0 + u * blockDim.x;
       if (i < nt) {
         bq[u] = reinterpret_cast<const int4 *>(bd)[i];
-        if (upd) {
+        if (upd && tail_only) {  // the (all-reduced) partial: votes, fixed-point A
+          vq[u] = (int)p.partial[(int64_t)b * 2 * MS + i];
+          aq[u] = p.partial[(int64_t)b * 2 * MS + MS + i];
+        } else if (upd) {
           vq[u] = __ldcg(&p.ws_votes[(int64_t)b * MS + i]);
           aq[u] = __ldcg(&p.ws_a[(int64_t)b * MS + i]);
         } else {
@@ -210,8 +256,10 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
         if (upd) {
           v[i] = vq[u];
           A[i] = aq[u];
-          p.ws_votes[(int64_t)b * MS + i] = 0;
-          p.ws_a[(int64_t)b * MS + i] = 0;
+          if (!tail_only) {
+            p.ws_votes[(int64_t)b * MS + i] = 0;
+            p.ws_a[(int64_t)b * MS + i] = 0;
+          }
         } else {
           fl[i] = (uint8_t)vq[u];
         }
@@ -220,14 +268,14 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   }
   __syncthreads();
   if (upd) {
-  if (p.partial) {
+  if (p.partial && !tail_only) {
     int64_t *pv = p.partial + (int64_t)b * 2 * MS;
     for (int i = threadIdx.x; i < MS; i += blockDim.x) {
       pv[i] = i < nt ? v[i] : 0;
       pv[MS + i] = i < nt ? A[i] : 0;
     }
   }
-  if (p.stop_after == 2) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
+  if (p.stop_after == 2 || p.mode == kFront) { if (threadIdx.x == 0) p.ws_ticket[b] = 0; return; }
   if (threadIdx.x == 0) TL(3);
   // ---- a3: consensus top-c ----------------------------------------------------------
   block_topc(v, A, nt, p.c, fl, hist, grp, scratch, p.agreeability ? p.agreeability + b : nullptr);
@@ -249,7 +297,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
                       p.cap, p.count + b, grp, scratch, p.status,
                       p.index_phys ? p.index_phys + (int64_t)b * p.cap : nullptr, pts, p.P, p.Hkv * p.P);
   }
-  if (threadIdx.x == 0) p.ws_ticket[b] = 0;  // ready for the next step
+  if (threadIdx.x == 0 && !tail_only) p.ws_ticket[b] = 0;  // ready for the next step
   __syncthreads();
   if (threadIdx.x == 0) TL(5);
 }
@@ -271,6 +319,12 @@ extern "C" size_t zoomr_select_workspace_bytes(const zoomr_geom *geom, int32_t b
   return (size_t)batch * max_summaries * (8 + 4) + (size_t)batch * 4 + 256;
 }
 
+#ifdef ZOOMR_AB_NO_COOP  // A/B builds only: the last-arriving CTA runs a3/a4 (no cooperative launch)
+constexpr bool kDesignatedTail = false;
+#else
+constexpr bool kDesignatedTail = true;
+#endif
+
 static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
                         const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
                         const uint8_t *update,
@@ -278,22 +332,33 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
                         int64_t *partial, uint8_t *flags, float *agreeability, int32_t *index,
                         int32_t *index_phys, int32_t index_capacity, int32_t *index_count, float *alpha_out,
                         int32_t *topk_out, void *workspace, size_t workspace_bytes,
-                        int32_t *dev_status, void *stream, bool chained) {
+                        int32_t *dev_status, void *stream, bool chained, int mode = kFull) {
   int rc = check_geom(geom);
   if (rc) return rc;
-  if (batch < 1 || !q || !kv || !kv->k || !kv->page_table || !seg || !seg->bounds || !seg->num_summaries ||
-      !seg->seq_len || !mean_keys || !flags || !index || !index_count || index_capacity < 1 || top_k < 1 ||
-      c < 0 || sink < 0 || window < 1 || n_close < 0 || (n_close > 0 && !close_items) || !workspace ||
-      seg->max_summaries < 1 || kv->num_pages < 1 || kv->max_pages < 1)
+  if (batch < 1 || !seg || !seg->bounds || !seg->num_summaries || !seg->seq_len || seg->max_summaries < 1)
     return ZOOMR_ERR_INVALID_ARG;
-  if (top_k > kMaxTopK || seg->max_summaries > kMaxSummaries) return ZOOMR_ERR_UNSUPPORTED;
-  if (workspace_bytes < zoomr_select_workspace_bytes(geom, batch, seg->max_summaries)) return ZOOMR_ERR_WORKSPACE;
+  const bool front = mode != kTail, back = mode != kFront;  // runs a1 + a2 / runs a3 + a4
+  if (front && (!q || !kv || !kv->k || !kv->page_table || kv->num_pages < 1 || kv->max_pages < 1 || !mean_keys ||
+                top_k < 1 || n_close < 0 || (n_close > 0 && !close_items) || !workspace))
+    return ZOOMR_ERR_INVALID_ARG;
+  if (back && (!flags || !index || !index_count || index_capacity < 1 || c < 0 || sink < 0 || window < 1))
+    return ZOOMR_ERR_INVALID_ARG;
+  if (mode != kFull && !partial) return ZOOMR_ERR_INVALID_ARG;  // the front's output / the tail's input
+  if (index_phys && (!kv || !kv->page_table || kv->max_pages < 1)) return ZOOMR_ERR_INVALID_ARG;
+  if ((front && top_k > kMaxTopK) || seg->max_summaries > kMaxSummaries) return ZOOMR_ERR_UNSUPPORTED;
+  if (front && workspace_bytes < zoomr_select_workspace_bytes(geom, batch, seg->max_summaries))
+    return ZOOMR_ERR_WORKSPACE;
+  if (!front) {
+    top_k = 1;  // unused by the tail; keeps the shared-memory sizing valid
+    n_close = 0;
+  }
   FusedParams p;
+  p.mode = mode;
   p.q = (const __nv_bfloat16 *)q;
-  p.kpool = (const __nv_bfloat16 *)kv->k;
-  p.num_pages = kv->num_pages;
-  p.page_table = kv->page_table;
-  p.max_pages = kv->max_pages;
+  p.kpool = kv ? (const __nv_bfloat16 *)kv->k : nullptr;
+  p.num_pages = kv ? kv->num_pages : 0;
+  p.page_table = kv ? kv->page_table : nullptr;
+  p.max_pages = kv ? kv->max_pages : 1;
   p.bounds = seg->bounds;
   p.num_summaries = seg->num_summaries;
   p.seq_len = seg->seq_len;
@@ -336,11 +401,12 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   }
 #endif
   const int G = geom->num_q_heads / geom->num_kv_heads;
-  dim3 grid(geom->num_layers * geom->num_kv_heads, batch);
+  dim3 grid(mode == kTail ? 1 : geom->num_layers * geom->num_kv_heads, batch);
+  const int max_pages = p.max_pages;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
     auto kfn = fused_select_kernel<DD, GG>;                                                      \
-    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, kv->max_pages);                     \
+    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, max_pages);         \
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     prefer_max_smem(kfn);                                                                        \
@@ -349,7 +415,9 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
     /* the designated tail spins on its siblings: only under a cooperative launch, which      \
        guarantees that the whole grid is resident at once (never in the chained variant,      \
        whose CTAs may wait for SMs still held by the preceding a5) */                          \
-    p.designated_tail = !p.pdl_front && (int64_t)grid.x * grid.y <= (int64_t)per_sm * num_sms(); \
+    p.designated_tail = kDesignatedTail && mode != kTail && !p.pdl_front &&                     \
+                        (int64_t)(grid.x + 1) * grid.y <= (int64_t)per_sm * num_sms();           \
+    if (p.designated_tail) grid.x += 1; /* + the tail CTA of each sequence */                   \
     if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                                     \
     else if (p.designated_tail) launch_cooperative(kfn, grid, 256, smem, s, p);                  \
     else kfn<<<grid, 256, smem, s>>>(p);                                                         \
@@ -387,3 +455,23 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
 extern "C" int zoomr_select_fused(ZOOMR_SELECT_FUSED_ARGS) { return ZOOMR_SELECT_FUSED_CALL(false); }
 
 extern "C" int zoomr_select_fused_chained(ZOOMR_SELECT_FUSED_ARGS) { return ZOOMR_SELECT_FUSED_CALL(true); }
+
+extern "C" int zoomr_select_front(const zoomr_geom *geom, int32_t batch, const void *q, const zoomr_kv *kv,
+                                  const zoomr_segments *seg, const int32_t *close_items, int32_t n_close,
+                                  const uint8_t *update, float *mean_keys, int32_t top_k, int64_t *partial,
+                                  float *alpha_out, int32_t *topk_out, void *workspace, size_t workspace_bytes,
+                                  int32_t *dev_status, void *stream) {
+  return select_fused(geom, batch, q, kv, seg, close_items, n_close, update, mean_keys, top_k, 0, 0, 1, partial,
+                      nullptr, nullptr, nullptr, nullptr, 0, nullptr, alpha_out, topk_out, workspace, workspace_bytes,
+                      dev_status, stream, false, kFront);
+}
+
+extern "C" int zoomr_select_tail(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const zoomr_segments *seg,
+                                 const int64_t *partial, const uint8_t *update, int32_t c, int32_t sink,
+                                 int32_t window, uint8_t *flags, float *agreeability, int32_t *index,
+                                 int32_t *index_phys, int32_t index_capacity, int32_t *index_count,
+                                 int32_t *dev_status, void *stream) {
+  return select_fused(geom, batch, nullptr, kv, seg, nullptr, 0, update, nullptr, 1, c, sink, window,
+                      const_cast<int64_t *>(partial), flags, agreeability, index, index_phys, index_capacity,
+                      index_count, nullptr, nullptr, nullptr, 0, dev_status, stream, false, kTail);
+}

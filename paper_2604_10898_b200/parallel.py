@@ -108,8 +108,10 @@ class HeadShardedStep(ZoomrStep):
         self.global_shape, self.shard = shape, shard
         self._ar = nccl_allreduce_sum(group)
 
-    def run(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=False):
-        return super().run(q, kv, seg, update_selection, close_items, allreduce or self._ar, fused=False)
+    def run(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=True):
+        """fused (default): zoomr_select_front -> all-reduce -> zoomr_select_tail -> a5;
+        fused=False: the five separate calls with the all-reduce between a2 and a3."""
+        return super().run(q, kv, seg, update_selection, close_items, allreduce or self._ar, fused=fused)
 
 
 # ---------------------------------------------------------------- token sharding --

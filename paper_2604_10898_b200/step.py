@@ -100,6 +100,18 @@ class ZoomrStep:
                            chained=self.chained)
             self.attend(q, kv, seq_len, chained=self.chained)
             return self.out
+        if fused and update_selection:
+            # KV-head-sharded: a1 + a2 (zoomr_select_front) -> all-reduce of
+            # the partial -> a3 + a4 (zoomr_select_tail), then a5 (early rows overlap the tail)
+            Z.select_front(self.shape, q, k_pool, v_pool, page_table, bounds, nsum, seq_len,
+                           close_items if close_items is not None and close_items.numel() else None,
+                           self.mean_keys, p.top_k, self.partial, self.sel_workspace, alpha_out=self.alpha,
+                           topk_out=self.topk, dev_status=self.status)
+            allreduce(self.partial)
+            Z.select_tail(self.shape, bounds, nsum, seq_len, self.partial, p.c, p.sink, p.window, self.flags,
+                          self.index, self.count, agreeability=self.agreeability, dev_status=self.status)
+            self.attend(q, kv, seq_len, phys=False)
+            return self.out
         if close_items is not None and close_items.numel():
             self.update_mean_keys(kv, seg, close_items)
         if update_selection:
@@ -125,14 +137,15 @@ class ZoomrStep:
                              seq_len=seq_len if self.early_known else None, sink=p.sink, window=p.window,
                              chained=chained)
 
-    def launches_per_step(self, update_selection=True, close=False, fused=True) -> int:
-        """Kernel launches one run() enqueues (a2 = zero + score when not fused)."""
+    def launches_per_step(self, update_selection=True, close=False, fused=True, sharded=False) -> int:
+        """Kernel launches of libzoomr one run() enqueues (a2 = zero + score when not fused;
+        the head-sharded fused path: front + tail + a5, plus the caller's all-reduce)."""
         if fused and update_selection:
-            return 2
+            return 3 if sharded else 2
         return (1 if close else 0) + (3 if update_selection else 0) + 2
 
-    def capture(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=True):
-        """Capture run() into a CUDA graph (one launch per step afterwards)."""
+    def capture(self, q, kv, seg, update_selection=True, close_items=None, allreduce=None, fused=True, steps=1):
+        """Capture `steps` back-to-back run()s into a CUDA graph (one launch per replay)."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -141,7 +154,8 @@ class ZoomrStep:
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.run(q, kv, seg, update_selection, close_items, allreduce, fused)
+            for _ in range(steps):
+                self.run(q, kv, seg, update_selection, close_items, allreduce, fused)
         return g
 
     def check_status(self):

@@ -27,7 +27,7 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
            "zoomr_write_newest_kv", "zoomr_sparse_decode_attn_chained", "zoomr_select_fused_chained",
-           "zoomr_status_str", "zoomr_abi_version")
+           "zoomr_select_front", "zoomr_select_tail", "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -78,6 +78,10 @@ def lib():
         L.zoomr_select_fused.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp,
                                          vp, vp, vp, i32, vp, vp, vp, vp, sz, vp, vp]
         L.zoomr_select_fused.restype = C.c_int
+        L.zoomr_select_front.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp, vp, sz, vp, vp]
+        L.zoomr_select_front.restype = C.c_int
+        L.zoomr_select_tail.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, i32, vp, vp, vp]
+        L.zoomr_select_tail.restype = C.c_int
         L.zoomr_append_kv.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_append_kv.restype = C.c_int
         L.zoomr_track_segments.argtypes = [i32, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp]
@@ -407,6 +411,38 @@ def select_fused(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summar
     _check("zoomr_select_fused", rc)
 
 
+def select_front(shape: Shape, q, k_pool, v_pool, page_table, bounds, num_summaries, seq_len, close_items,
+                 mean_keys, top_k, partial, workspace, alpha_out=None, topk_out=None, dev_status=None, update=None,
+                 stream=None):
+    """a1 + a2 with aggregation into partial int64 [B][2][max_summaries] (zoomr_select_front)."""
+    g, kv, sg = shape.c(), _kv(k_pool, v_pool, page_table), _seg(bounds, num_summaries, seq_len)
+    n_close = 0 if close_items is None else close_items.shape[0]
+    rc = lib().zoomr_select_front(
+        C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"), C.byref(kv), C.byref(sg),
+        _ptr(close_items, torch.int32, "close_items") if n_close else None, n_close,
+        _ptr(update, torch.uint8, "update"), _ptr(mean_keys, torch.float32, "mean_keys"), int(top_k),
+        _ptr(partial, torch.int64, "partial"), _ptr(alpha_out, torch.float32, "alpha_out"),
+        _ptr(topk_out, torch.int32, "topk_out"), _ptr(workspace, None, "workspace"),
+        workspace.numel() * workspace.element_size(), _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_select_front", rc)
+
+
+def select_tail(shape: Shape, bounds, num_summaries, seq_len, partial, c, sink, window, flags, index, index_count,
+                agreeability=None, dev_status=None, update=None, page_table=None, index_phys=None, stream=None):
+    """a3 + a4 from a (reduced) partial (zoomr_select_tail)."""
+    g, sg = shape.c(), _seg(bounds, num_summaries, seq_len)
+    kv = None
+    if index_phys is not None:
+        kv = KV(None, None, 1, _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
+    rc = lib().zoomr_select_tail(
+        C.byref(g), partial.shape[0], C.byref(kv) if kv is not None else None, C.byref(sg),
+        _ptr(partial, torch.int64, "partial"), _ptr(update, torch.uint8, "update"), int(c), int(sink), int(window),
+        _ptr(flags, torch.uint8, "flags"), _ptr(agreeability, torch.float32, "agreeability"),
+        _ptr(index, torch.int32, "index"), _ptr(index_phys, torch.int32, "index_phys"), index.shape[1],
+        _ptr(index_count, torch.int32, "index_count"), _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_select_tail", rc)
+
+
 def append_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_len, dev_status=None, stream=None):
     """a0 (zoomr_append_kv): rows k_new / v_new bf16 [B][L][H_kv][d] at position seq_len[b]; seq_len += 1.
     The pools may be pinned host tensors (the host tier)."""
@@ -442,7 +478,7 @@ def track_segments(token_ids, begin_id, end_id, boundary_ids, seq_len, bounds, n
 # ---- NVTX: one range per enqueued stage (host-side marks; visible to ncu --nvtx / nsys) ----------
 _STAGES = {
     "update_mean_keys": "a1", "score": "a2", "select_topc": "a3", "build_index": "a4",
-    "sparse_decode_attn": "a5", "select_fused": "a1-a4", "append_kv": "a0", "track_segments": "a0",
+    "sparse_decode_attn": "a5", "select_fused": "a1-a4", "select_front": "a1-a2", "select_tail": "a3-a4", "append_kv": "a0", "track_segments": "a0",
     "shard_index": "a4-shard", "sparse_decode_attn_lse": "a5-lse", "merge_attn": "a5-merge",
     "sparse_decode_attn_logits": "a5-logits", "h2o_accumulate": "h2o", "h2o_select": "h2o",
     "tier_fetch": "tier", "write_newest_kv": "a0-tier",

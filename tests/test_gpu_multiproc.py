@@ -75,7 +75,7 @@ def _init(rank, world, port):
     return dist
 
 
-def _head_worker(rank, world, port, name, outdir):
+def _head_worker(rank, world, port, name, outdir, fused=True):
     dist = _init(rank, world, port)
     from paper_2604_10898_b200 import zoomr as Z
     from paper_2604_10898_b200.parallel import HeadShardedStep, shard_heads, slice_heads
@@ -94,7 +94,7 @@ def _head_worker(rank, world, port, name, outdir):
     res = []
     for s in range(STEPS):
         q = _queries(inp, s)[:, :, sh.q_start:sh.q_stop].contiguous()
-        st.run(q, kv, seg, close_items=newest)  # a1 (newest) a2 -> all-reduce -> a3 a4 a5
+        st.run(q, kv, seg, close_items=newest, fused=fused)  # a1 (newest) a2 -> all-reduce -> a3 a4 a5
         torch.cuda.synchronize()
         st.check_status()
         res.append({k: getattr(st, k).cpu().clone() for k in ("partial", "flags", "index", "count", "out")})
@@ -141,10 +141,10 @@ def _token_worker(rank, world, port, name, outdir):
     dist.destroy_process_group()
 
 
-def _spawn(fn, world, name):
+def _spawn(fn, world, name, *extra):
     import torch.multiprocessing as mp
     d = tempfile.mkdtemp(prefix="zoomr_mp_")
-    mp.spawn(fn, args=(world, _free_port(), name, d), nprocs=world, join=True)
+    mp.spawn(fn, args=(world, _free_port(), name, d, *extra), nprocs=world, join=True)
     return d
 
 
@@ -163,10 +163,12 @@ def _oracle_steps(inp):
     return ref
 
 
-@pytest.mark.parametrize("name", ["small_g4", "8b16k"])
-def test_head_sharded_step_two_processes(name):
+@pytest.mark.parametrize("name,fused", [("small_g4", True), ("small_g4", False), ("8b16k", True)])
+def test_head_sharded_step_two_processes(name, fused):
+    """fused: zoomr_select_front -> all-reduce -> zoomr_select_tail -> a5 (the bench's
+    path); not fused: a1, a2, all-reduce, a3, a4, a5 as separate calls."""
     world = 2
-    d = _spawn(_head_worker, world, name)
+    d = _spawn(_head_worker, world, name, fused)
     inp = S.generate(CFGS[name], device="cuda")
     ref = _oracle_steps(inp)
     outs = [torch.load(os.path.join(d, f"head{r}.pt")) for r in range(world)]

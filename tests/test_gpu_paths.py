@@ -363,3 +363,61 @@ def test_a5_layer_ranges(ranges):
     with pytest.raises(Z.ZoomrError):
         Z.sparse_decode_attn(st.shape, inp.q, *kv, st.index, st.count, out, st.workspace, layer_begin=7,
                              layer_count=2)
+
+
+@pytest.mark.parametrize("cfg", [
+    _small("ft_b3", d=128, batch=3, jitter=True),
+    _small("ft_g7", d=128, Hq=14, Hkv=2),
+    dataclasses.replace(S.stress_config(64, 8), name="ft_stress_LR64", seed=16),
+], ids=lambda c: c.name)
+def test_select_front_tail_equal_separate_calls(cfg):
+    """zoomr_select_front + zoomr_select_tail (ABI 9, the KV-head-sharded step's
+    select around its all-reduce) == zoomr_score + zoomr_select_topc +
+    zoomr_build_index, bit for bit (partial, flags, AG, I_f), with and without the
+    front's a1 of the newest summaries, and with update[b] = 0 holding flags."""
+    from paper_2604_10898_b200 import zoomr as Z
+    inp = S.generate(cfg, device="cuda")
+    cap = 40000 if cfg.T > 4096 else None
+    kv = (inp.k_pool, inp.v_pool, inp.page_table)
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    ref = PY.make_step(inp, capacity=cap)
+    PY.run_full(inp, ref, fused=False)
+    st = PY.make_step(inp, capacity=cap)
+    st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
+    newest = torch.tensor([[b, int(n) - 1] for b, n in enumerate(inp.num_summaries.cpu().tolist())],
+                          dtype=torch.int32, device="cuda")
+    for b, i in newest.tolist():
+        st.mean_keys[b, :, :, i] = float("nan")  # the front's a1 must recompute them
+    for rep in range(2):
+        st.partial.fill_(-1)
+        Z.select_front(st.shape, inp.q, *kv, *seg, newest if rep == 0 else None, st.mean_keys, cfg.top_k,
+                       st.partial, st.sel_workspace, alpha_out=st.alpha, topk_out=st.topk, dev_status=st.status)
+        Z.select_tail(st.shape, *seg, st.partial, cfg.c, cfg.sink, cfg.window, st.flags, st.index, st.count,
+                      agreeability=st.agreeability, dev_status=st.status)
+        torch.cuda.synchronize()
+        st.check_status()
+        assert torch.equal(st.partial, ref.partial)
+        assert torch.equal(st.flags, ref.flags) and torch.equal(st.count, ref.count)
+        assert torch.equal(st.agreeability, ref.agreeability)
+        for b in range(inp.q.shape[0]):
+            n = int(st.count[b])
+            assert torch.equal(st.index[b, :n], ref.index[b, :n])
+        assert int(st.sel_workspace.count_nonzero()) == 0
+    # update[b] = 0: the front leaves partial[b] alone, the tail keeps flags[b] and rebuilds I_f
+    if inp.q.shape[0] > 1:
+        upd = torch.ones(inp.q.shape[0], dtype=torch.uint8, device="cuda")
+        upd[0] = 0
+        held = st.flags.clone()
+        st.flags[1:].zero_()
+        st.partial[0].fill_(-7)
+        q2 = (0.25 * torch.randn(inp.q.shape, device="cuda")).bfloat16()
+        Z.select_front(st.shape, q2, *kv, *seg, None, st.mean_keys, cfg.top_k, st.partial, st.sel_workspace,
+                       dev_status=st.status, update=upd)
+        Z.select_tail(st.shape, *seg, st.partial, cfg.c, cfg.sink, cfg.window, st.flags, st.index, st.count,
+                      dev_status=st.status, update=upd)
+        torch.cuda.synchronize()
+        st.check_status()
+        assert bool((st.partial[0] == -7).all())
+        assert torch.equal(st.flags[0], held[0])
+        n0 = int(st.count[0])
+        assert torch.equal(st.index[0, :n0], ref.index[0, :n0])

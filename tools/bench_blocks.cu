@@ -42,7 +42,8 @@ __global__ void k_index(const int *bdg, const uint8_t *flg, int nt, int T, int i
 }
 
 int main() {
-  const int nt = 120, T = 16384;
+  for (int nt : {120, 240}) {
+  const int T = 16384 * (nt / 120);
   std::vector<int> v(nt, 0), bd(nt * 4);
   std::vector<long long> a(nt, 0);
   std::vector<uint8_t> fl(nt, 1);
@@ -57,15 +58,18 @@ int main() {
   cudaMemcpy(dbd, bd.data(), nt * 16, cudaMemcpyHostToDevice); cudaMemcpy(dfl, fl.data(), nt, cudaMemcpyHostToDevice);
   long long h;
   for (int threads : {256, 512}) {
-    k_topc<<<1, threads, 32 * 1024>>>(dv, da, nt, 4, 50, dout); cudaDeviceSynchronize();
-    cudaMemcpy(&h, dout, 8, cudaMemcpyDeviceToHost);
-    printf("threads %d: block_topc(nt=%d, c=4) %lld cycles\n", threads, nt, h);
+    for (int c : {4, 9}) {
+      k_topc<<<1, threads, 32 * 1024>>>(dv, da, nt, c, 50, dout); cudaDeviceSynchronize();
+      cudaMemcpy(&h, dout, 8, cudaMemcpyDeviceToHost);
+      printf("threads %d: block_topc(nt=%d, c=%d%s) %lld cycles\n", threads, nt, c, c <= kTopcRounds ? ", rounds" : "", h);
+    }
     for (int cap : {1 << 16, 1}) {
       k_index<<<1, threads, 32 * 1024>>>(dbd, dfl, nt, T, 50, didx, dcnt, dout, cap); cudaDeviceSynchronize();
       cudaMemcpy(&h, dout, 8, cudaMemcpyDeviceToHost);
       int c; cudaMemcpy(&c, dcnt, 4, cudaMemcpyDeviceToHost);
       printf("threads %d: block_build_index(nt=%d, cap %d) %lld cycles (count %d) %s\n", threads, nt, cap, h, c, cudaGetErrorString(cudaGetLastError()));
     }
+  }
   }
   return 0;
 }

@@ -13,6 +13,9 @@ from paper_2604_10898_b200 import zoomr as Z
 from paper_2604_10898_b200.step import StepParams, ZoomrStep
 
 cfg = S.config_by_name(os.environ.get("WL", "8b16k"))
+if os.environ.get("HKV"):  # a head shard's geometry (e.g. HKV=1 HQ=8 for one rank of 70B-64K over 8)
+    import dataclasses
+    cfg = dataclasses.replace(cfg, Hkv=int(os.environ["HKV"]), Hq=int(os.environ["HQ"]))
 shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
 lib = Z.lib()
 for fn in ("zoomr_tl_arm_fused", "zoomr_tl_arm_attn"):

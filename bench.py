@@ -505,6 +505,68 @@ def head_sharded_section(rank, world, K, W, hbm):
     return res
 
 
+def layer_pipelined_section(shape, prm, s0, cfg, host_k, host_v, cache_bytes):
+    from oracle.transfer import simulate_transfer_schedule
+    from paper_2604_10898_b200.tier import LayerPipelinedTierStep
+    inp = s0["inp"]
+    seg = s0["seg"]
+    out = {}
+
+    def g_time(fn, n=3):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) * 1e3
+            best = t if best is None else min(best, t)
+        return best
+    for lg in (1, 4):
+        # slices sized for |I_f| <= 4096 rows (C2's largest |I_f| is 2836): a step with more reports CAPACITY
+        st = LayerPipelinedTierStep(shape, inp.bounds.shape[1], 4096, prm, host_k, host_v, inp.page_table,
+                                    layers_per_slice=lg)
+        st.mean_keys.copy_(s0["st"].mean_keys)
+        st.run(inp.q, seg)
+        torch.cuda.synchronize()
+        st.check_status()
+        ng = cfg.L // lg
+        t_sel = g_time(lambda: st.select(inp.q, seg))
+        t_in = [g_time(lambda g=g: st.gather(g)) for g in range(ng)]
+        t_c = [g_time(lambda g=g: st.attend_group(inp.q, g)) for g in range(ng)]
+        t_pipe = g_time(lambda: st.run(inp.q, seg))
+        t_serial = g_time(lambda: st.run(inp.q, seg, pipelined=False))
+        sim = simulate_transfer_schedule(t_in, t_c)
+        cnt = int(st.count[0])
+        slice_bytes = cnt * lg * cfg.Hkv * cfg.d * 2 * 2
+        st.check_status()
+        out[f"layers_per_slice_{lg}"] = {
+            "step_us_pipelined": t_pipe, "step_us_serial": t_serial, "select_us": t_sel,
+            "gather_us_per_group_mean": sum(t_in) / ng, "attend_us_per_group_mean": sum(t_c) / ng,
+            "model_total_us": t_sel + sim["total_time"], "model_serial_us": t_sel + sim["serial_time"],
+            "model_vs_measured_pipelined": (t_sel + sim["total_time"]) / t_pipe,
+            "model_peak_resident_slices": sim["peak_resident_layers"],
+            "host_link_gbs": slice_bytes / (sum(t_in) / ng * 1e-6) / 1e9,
+            "hbm_bytes": st.hbm_bytes(), "hbm_saving": cache_bytes / st.hbm_bytes(), "index_count": cnt}
+        del st
+    out["note"] = ("the paper's system: each step reloads I_f's rows layer group by layer group from pinned host "
+                   "memory (SM-driven zero-copy gather) into one of two HBM slices while the previous group attends; "
+                   "model = select + SPEC simulate_transfer_schedule(measured per-group gather, attend times)")
+    return out
+
+
 def host_tier_section(shape, prm, s0, cfg, K, hot_page_sizes=(64, 16)):
     """NEXT-2: the cache in pinned host memory, an HBM hot pool caching its pages."""
     from paper_2604_10898_b200.tier import HostTierStep
@@ -600,6 +662,12 @@ def host_tier_section(shape, prm, s0, cfg, K, hot_page_sizes=(64, 16)):
     res["decode_loop_us_per_token"] = loop_run()
     lp.check_status()
     del lp, gl_
+    # the paper's own transfer schedule: per step, the rows of I_f of each layer
+    # group gathered host -> HBM slice on a copy stream while the previous group attends,
+    # two slices resident; checked against SPEC's transfer-schedule model (oracle/transfer.py)
+    # fed with the per-group transfer and compute times measured here
+    if B == 1:
+        res["paper_layer_pipelined"] = layer_pipelined_section(shape, prm, s0, cfg, host_k, host_v, cache_bytes)
     hb = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     db = torch.empty_like(hb, device="cuda")
     res["host_link_memcpy_gbs"] = hb.numel() / (ev_time(lambda: db.copy_(hb, non_blocking=True), 5) * 1e-6) / 1e9

@@ -338,6 +338,26 @@ int zoomr_track_segments(int32_t batch, const int32_t *token_ids, int32_t begin_
                          int32_t *bounds, int32_t *num_summaries, int32_t max_summaries, int32_t *state,
                          int32_t *close_items, uint8_t *update, int32_t *dev_status, void *stream);
 
+/* The paper's transfer unit, layer by layer ("For each layer of the
+ * model, the required KV cache slices are transferred to the GPU ... while the
+ * KVs for the next layer are prefetched"): copies the rows
+ * of I_f (index / index_count as a4 writes them) of layers [layer_begin,
+ * layer_begin + layer_count), every KV head, K and V, from the host cache
+ * (host_kv: pinned host pools read through their unified address, bf16
+ * [L][num_pages][H_kv][P][d], device page table) into the slice buffers
+ * slice_k / slice_v, device bf16 [layer_count][B * slice_pages_per_seq][H_kv]
+ * [slice_page_size][d]: row j of sequence b lands in slice page
+ * b * slice_pages_per_seq + j / slice_page_size, slot j % slice_page_size.  The
+ * slice is then a pool that a5 attends with the identity page table and the
+ * index 0 .. count-1 (positions are irrelevant to attention).
+ * slice_page_size * slice_pages_per_seq >= index_capacity.  Launched with PDL:
+ * the index is read after the preceding kernel completed.  Device errors:
+ * INDEX_RANGE (a position without a host page). */
+int zoomr_tier_gather_slice(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, const int32_t *index,
+                            const int32_t *index_count, int32_t index_capacity, int32_t layer_begin,
+                            int32_t layer_count, void *slice_k, void *slice_v, int32_t slice_page_size,
+                            int32_t slice_pages_per_seq, int32_t *dev_status, void *stream);
+
 /* ---- Token-sharded split-K across GPUs (H_kv < #GPUs) --------
  *
  * The KV cache of a sequence is spread over R ranks by token (owner[b][t] = the
@@ -453,11 +473,15 @@ int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *pr
  * CAPACITY (the hot pool cannot hold the pages of this step's I_f; the rest
  * stay missing), INDEX_RANGE. */
 size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t hot_pages);
+/* k_new, v_new (nullable, bf16 [B][L][H_kv][d]) + seq_len: also write the
+ * newest token's rows (position seq_len[b] - 1, resident since I_w holds it)
+ * into the hot pool -- what zoomr_write_newest_kv does, without a launch of its
+ * own (ABI 9); the host cache must already hold them (zoomr_append_kv). */
 int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k, void *hot_v,
                      int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table, int32_t *hot_owner,
                      int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
-                     int32_t index_capacity, void *workspace, size_t workspace_bytes, int32_t *dev_status,
-                     void *stream);
+                     int32_t index_capacity, const void *k_new, const void *v_new, const int32_t *seq_len,
+                     void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

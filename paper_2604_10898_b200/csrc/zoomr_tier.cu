@@ -60,6 +60,10 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
   __shared__ int hist[256];
   __shared__ unsigned long long s_prefix;
   __shared__ int s_need;
+  // launched with PDL behind the select: the copy kernel may launch now (it waits
+  // for this plan), and I_f / its count are read only after the select completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x;
   const int hmp = max_pages * R;
   const int NP = B * hmp;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
   // 3. victims: the nmiss least recently used hot pages this step does not touch
   //    (free pages have stamp -1); key (stamp + 1, page) -- unique
   int ncand = 0;
-  for (int h0 = 0; h0 < hot_pages; h0 += kPlanThreads) {
+  for (int h0 = 0; h0 < hot_pages && nmiss > 0; h0 += kPlanThreads) {  // (warm step: nothing missing, no search)
     const int h = h0 + tid;
     int tot;
     tier_block_scan((h < hot_pages && stamp[h] < step) ? 1 : 0, wsum, &tot);
@@ -203,8 +207,37 @@ __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict_
                                                          const uint4 *__restrict__ host_v, int64_t host_pages,
                                                          uint4 *__restrict__ hot_k, uint4 *__restrict__ hot_v,
                                                          int64_t hot_pages, int32_t L, int32_t Hkv, int32_t R,
-                                                         int32_t row16, const int32_t *__restrict__ ws, int32_t NP) {
+                                                         int32_t row16, const int32_t *__restrict__ ws, int32_t NP,
+                                                         const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                                                         const int32_t *__restrict__ seq_len,
+                                                         const int32_t *__restrict__ hot_pt, int32_t hmp, int32_t Ph,
+                                                         int32_t B, int32_t *status) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a5 may launch (it waits for this copy)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the newest token's rows (k_new / v_new [B][L][H_kv][d]) into its hot page -- resident,
+  // since I_w holds position T-1.  The host cache already holds the same rows
+  // (zoomr_append_kv wrote them before the selection), so a concurrent copy of
+  // that page below writes identical bytes.
+  if (k_new) {
+    const int rowu = row16 / Ph;  // uint4 per (token, head) row
+    for (int64_t w = blockIdx.x; w < (int64_t)B * L; w += gridDim.x) {
+      const int b = (int)(w / L), l = (int)(w - (int64_t)b * L);
+      const int pos = seq_len[b] - 1;
+      const int lp = pos / Ph;
+      const int hp = (pos >= 0 && lp < hmp) ? hot_pt[(int64_t)b * hmp + lp] : -1;
+      if (hp < 0 || hp >= hot_pages) {
+        if (threadIdx.x == 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
+        continue;
+      }
+      for (int e = threadIdx.x; e < Hkv * rowu; e += blockDim.x) {
+        const int g = e / rowu, c = e - g * rowu;
+        const int64_t dst = (((int64_t)l * hot_pages + hp) * Hkv + g) * row16 + (int64_t)(pos - lp * Ph) * rowu + c;
+        const int64_t src = (((int64_t)b * L + l) * Hkv + g) * rowu + c;
+        hot_k[dst] = k_new[src];
+        hot_v[dst] = v_new[src];
+      }
+    }
+  }
   const int nf = ws[1];
   const int32_t *fetch_hot = ws + 2 + NP + hot_pages, *fetch_host = fetch_hot + hot_pages;
   const int64_t items = (int64_t)nf * L * 2;
@@ -237,9 +270,92 @@ __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict_
   }
 }
 
+// The paper's own transfer unit: the rows of I_f of one group of
+// layers, gathered from the host cache into an HBM slice laid out as a small
+// pool [layer_count][B * spp][H_kv][Ps][d]: row j of sequence b sits in slice
+// page b * spp + j / Ps, slot j % Ps (spp = slice pages per sequence).  Work
+// item = (layer, sequence, 8 consecutive rows of I_f, K or V); a warp moves one
+// (row, head) run of 2*d bytes per 16-byte lane group, four host reads in
+// flight per thread.  Launched with PDL: the index is read after the wait.
+constexpr int kSliceRows = 8;
+__global__ void __launch_bounds__(256) tier_gather_slice_kernel(
+    const __nv_bfloat16 *__restrict__ host_k, const __nv_bfloat16 *__restrict__ host_v, int64_t host_pages,
+    const int32_t *__restrict__ page_table, int32_t max_pages, const int32_t *__restrict__ index,
+    const int32_t *__restrict__ count, int32_t cap, int32_t B, int32_t L, int32_t Hkv, int32_t P, int32_t D,
+    int32_t l0, int32_t Lc, __nv_bfloat16 *__restrict__ slice_k, __nv_bfloat16 *__restrict__ slice_v, int32_t Ps,
+    int32_t spp, int32_t *status) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int c16 = D / 8;                  // 16-byte chunks of one (row, head)
+  const int per_item = kSliceRows * Hkv * c16;
+  const int64_t blocks_per_seq = (cap + kSliceRows - 1) / kSliceRows;
+  const int64_t items = (int64_t)Lc * B * blocks_per_seq * 2;
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int kv = (int)(w & 1);
+    int64_t r = w >> 1;
+    const int64_t blk = r % blocks_per_seq;
+    r /= blocks_per_seq;
+    const int b = (int)(r % B), ll = (int)(r / B), l = l0 + ll;
+    int n = count[b];
+    n = n < cap ? n : cap;
+    const int j0 = (int)blk * kSliceRows;
+    if (j0 >= n) continue;
+    const __nv_bfloat16 *src = kv ? host_v : host_k;
+    __nv_bfloat16 *dst = kv ? slice_v : slice_k;
+    for (int e0 = threadIdx.x; e0 < per_item; e0 += 4 * 256) {
+      uint4 val[4];
+      int64_t dsto[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * 256;
+        dsto[u] = -1;
+        if (e >= per_item) continue;
+        const int c = e % c16, gh = (e / c16) % Hkv, jr = e / (c16 * Hkv);
+        const int j = j0 + jr;
+        if (j >= n) continue;
+        const int t = index[(int64_t)b * cap + j];
+        const int lp = t / P;
+        const int page = (t >= 0 && lp < max_pages) ? page_table[(int64_t)b * max_pages + lp] : -1;
+        if (page < 0 || page >= host_pages) {
+          set_status(status, ZOOMR_ERR_INDEX_RANGE);
+          continue;
+        }
+        const int64_t so = ((((int64_t)l * host_pages + page) * Hkv + gh) * P + (t - lp * P)) * D + c * 8;
+        val[u] = __ldcs(reinterpret_cast<const uint4 *>(src + so));
+        const int sp = b * spp + j / Ps;
+        dsto[u] = ((((int64_t)ll * B * spp + sp) * Hkv + gh) * Ps + (j % Ps)) * D + c * 8;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (dsto[u] >= 0) *reinterpret_cast<uint4 *>(dst + dsto[u]) = val[u];
+    }
+  }
+}
+
 }  // namespace zoomr
 
 using namespace zoomr;
+
+extern "C" int zoomr_tier_gather_slice(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv,
+                                       const int32_t *index, const int32_t *index_count, int32_t index_capacity,
+                                       int32_t layer_begin, int32_t layer_count, void *slice_k, void *slice_v,
+                                       int32_t slice_page_size, int32_t slice_pages_per_seq, int32_t *dev_status,
+                                       void *stream) {
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (batch < 1 || !host_kv || !host_kv->k || !host_kv->v || !host_kv->page_table || host_kv->num_pages < 1 ||
+      host_kv->max_pages < 1 || !index || !index_count || index_capacity < 1 || !slice_k || !slice_v ||
+      slice_page_size < 1 || layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > geom->num_layers)
+    return ZOOMR_ERR_INVALID_ARG;
+  if ((int64_t)slice_page_size * slice_pages_per_seq < index_capacity) return ZOOMR_ERR_INVALID_ARG;
+  if (geom->head_dim % 8) return ZOOMR_ERR_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_pdl(tier_gather_slice_kernel, 4 * num_sms(), 256, 0, s, (const __nv_bfloat16 *)host_kv->k,
+             (const __nv_bfloat16 *)host_kv->v, (int64_t)host_kv->num_pages, host_kv->page_table, host_kv->max_pages,
+             index, index_count, index_capacity, batch, geom->num_layers, geom->num_kv_heads, geom->page_size,
+             geom->head_dim, layer_begin, layer_count, (__nv_bfloat16 *)slice_k, (__nv_bfloat16 *)slice_v,
+             slice_page_size, slice_pages_per_seq, dev_status);
+  return launch_status(s);
+}
 
 extern "C" size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t hot_pages) {
   if (batch < 1 || hot_max_pages < 1 || hot_pages < 1) return 0;
@@ -250,13 +366,13 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
                                 void *hot_v, int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table,
                                 int32_t *hot_owner,
                                 int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
-                                int32_t index_capacity, void *workspace, size_t workspace_bytes,
-                                int32_t *dev_status, void *stream) {
+                                int32_t index_capacity, const void *k_new, const void *v_new, const int32_t *seq_len,
+                                void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !host_kv || !host_kv->k || !host_kv->v || !host_kv->page_table || host_kv->num_pages < 1 ||
       host_kv->max_pages < 1 || !hot_k || !hot_v || hot_pages < 1 || !hot_page_table || !hot_owner || !hot_stamp ||
-      !index || !index_count || index_capacity < 1 || !workspace)
+      !index || !index_count || index_capacity < 1 || !workspace || (k_new && (!v_new || !seq_len)))
     return ZOOMR_ERR_INVALID_ARG;
   const int P = geom->page_size, Ph = hot_page_size;
   if (Ph < 1 || P % Ph) return ZOOMR_ERR_INVALID_ARG;
@@ -267,13 +383,15 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
   const int64_t row = (int64_t)Ph * geom->head_dim * 2;  // bytes of one (page, layer, head) block of the hot pool
   if (row % 16) return ZOOMR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
-  tier_plan_kernel<<<1, kPlanThreads, 0, s>>>(batch, index, index_count, index_capacity, Ph, R, host_kv->max_pages,
-                                              host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
-                                              (int32_t *)workspace, dev_status);
+  launch_pdl(tier_plan_kernel, 1, kPlanThreads, 0, s, batch, index, index_count, index_capacity, Ph, R,
+             host_kv->max_pages, host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
+             (int32_t *)workspace, dev_status);
   rc = launch_status(s);
   if (rc) return rc;
   launch_pdl(tier_copy_kernel, 2 * num_sms(), 256, 0, s, (const uint4 *)host_kv->k, (const uint4 *)host_kv->v,
              (int64_t)host_kv->num_pages, (uint4 *)hot_k, (uint4 *)hot_v, (int64_t)hot_pages, geom->num_layers,
-             geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp));
+             geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp),
+             (const uint4 *)k_new, (const uint4 *)v_new, seq_len, (const int32_t *)hot_page_table, (int32_t)hmp, Ph,
+             batch, dev_status);
   return launch_status((cudaStream_t)stream);
 }

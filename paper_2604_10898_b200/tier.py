@@ -84,8 +84,8 @@ class TierDecodeLoop(HostTierStep):
         segment tracking          zoomr_track_segments
         a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
                                   the host cache; a2/a3 only at semantic boundaries)
-        tier fetch                zoomr_tier_fetch (pages that entered I_f)
-        newest rows -> hot pool   zoomr_write_newest_kv (its page is resident: I_w holds T-1)
+        tier fetch                zoomr_tier_fetch (pages that entered I_f, and the newest
+                                  rows into their hot page: resident, I_w holds T-1)
         a5                        zoomr_sparse_decode_attn_lse on the hot pool
     """
 
@@ -134,10 +134,112 @@ class TierDecodeLoop(HostTierStep):
                        self.index, self.count, self.sel_workspace, partial=self.partial,
                        agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
                        dev_status=self.status, update=self.update)
+        # the fetch also writes the newest rows into their (resident) hot page
         Z.tier_fetch(hs, self.host_k, self.host_v, self.page_table, self.hot_k, self.hot_v, self.hot_page_table,
-                     self.hot_owner, self.hot_stamp, self.index, self.count, self.tier_ws, self.status)
-        Z.write_newest_kv(self.shape, self.hot_k, self.hot_v, self.hot_page_table, k_new, v_new, self.seq_len,
-                          self.status)
+                     self.hot_owner, self.hot_stamp, self.index, self.count, self.tier_ws, self.status,
+                     k_new=k_new, v_new=v_new, seq_len=self.seq_len)
         Z.sparse_decode_attn_lse(self.shape, q, self.hot_k, self.hot_v, self.hot_page_table, self.index, self.count,
                                  self.out, self.lse, self.workspace, dev_status=self.status)
         return self.out
+
+
+class LayerPipelinedTierStep(ZoomrStep):
+    """The paper's own system, as P:105-109 describes it:
+    the whole cache in (pinned) host memory; each step, after the selection,
+    "for each layer of the model, the required KV cache slices are transferred
+    to the GPU" and "the KVs for the next layer are prefetched" while the layer
+    attends.  Per group of `layers_per_slice` layers:
+
+        copy stream     zoomr_tier_gather_slice (rows of I_f, host -> HBM slice)
+        compute stream  a5 on the slice (identity page table, index 0..|I_f|-1)
+
+    with two slice buffers (peak residency: the slice being attended + the one
+    being prefetched), events ordering every reuse.  The new
+    token's K/V reach the host cache through zoomr_append_kv (write-through,
+    TierDecodeLoop) -- in this step-level class the cache is given.  Batch 1,
+    the paper's setting (q / out of a layer group are then contiguous views).
+    pipelined=False runs the same launches back to back on one stream (the
+    serial schedule SPEC's simulator compares against).
+    """
+
+    def __init__(self, shape: Z.Shape, max_summaries: int, index_capacity: int, params: StepParams,
+                 host_k: torch.Tensor, host_v: torch.Tensor, page_table: torch.Tensor, layers_per_slice: int = 1,
+                 slice_page_size: int = 64, device="cuda"):
+        super().__init__(shape, 1, max_summaries, index_capacity, params, device, early_known=False)
+        if not (host_k.is_pinned() and host_v.is_pinned()):
+            raise TypeError("the host tier needs pinned host tensors")
+        L, Hq, Hkv, d = shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
+        if L % layers_per_slice:
+            raise ValueError("layers_per_slice must divide the layer count")
+        dev = self.out.device
+        self.host_k, self.host_v, self.page_table = host_k, host_v, page_table
+        self.Lg, self.Ps = layers_per_slice, slice_page_size
+        spp = (index_capacity + slice_page_size - 1) // slice_page_size
+        self.slices = [(torch.zeros(self.Lg, spp, Hkv, slice_page_size, d, dtype=torch.bfloat16, device=dev),
+                        torch.zeros(self.Lg, spp, Hkv, slice_page_size, d, dtype=torch.bfloat16, device=dev))
+                       for _ in range(2)]
+        self.slice_pt = torch.arange(spp, dtype=torch.int32, device=dev).view(1, spp)
+        self.iota = torch.arange(index_capacity, dtype=torch.int32, device=dev).view(1, index_capacity)
+        self.slice_shape = Z.Shape(self.Lg, Hq, Hkv, d, slice_page_size)
+        self.slice_ws = [torch.zeros(max(Z.attn_workspace_bytes(self.slice_shape, 1), 1), dtype=torch.uint8,
+                                     device=dev) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        ng = L // self.Lg
+        self.ev_ready = [torch.cuda.Event() for _ in range(ng)]
+        self.ev_free = [torch.cuda.Event() for _ in range(ng)]
+
+    def hbm_bytes(self) -> int:
+        """HBM the tier needs besides q / out: the two slices + the mean-key cache + index."""
+        return sum(t.numel() * t.element_size() for pair in self.slices for t in pair) + \
+            self.mean_keys.numel() * 4 + self.index.numel() * 4
+
+    def select(self, q, seg, close_items=None):
+        bounds, nsum, seq_len = seg
+        p = self.params
+        Z.select_fused(self.shape, q, self.host_k, self.host_v, self.page_table, bounds, nsum, seq_len,
+                       close_items if close_items is not None and close_items.numel() else None, self.mean_keys,
+                       p.top_k, p.c, p.sink, p.window, self.flags, self.index, self.count, self.sel_workspace,
+                       partial=self.partial, agreeability=self.agreeability, dev_status=self.status)
+
+    def gather(self, g, stream=None):
+        sk, sv = self.slices[g % 2]
+        Z.tier_gather_slice(self.shape, self.host_k, self.host_v, self.page_table, self.index, self.count,
+                            g * self.Lg, self.Lg, sk, sv, dev_status=self.status, stream=stream)
+
+    def attend_group(self, q, g, stream=None):
+        sk, sv = self.slices[g % 2]
+        a, b = g * self.Lg, (g + 1) * self.Lg
+        Z.sparse_decode_attn(self.slice_shape, q[:, a:b], sk, sv, self.slice_pt, self.iota, self.count,
+                             self.out[:, a:b], self.slice_ws[g % 2], dev_status=self.status, stream=stream)
+
+    def run(self, q, seg, update_selection: bool = True, close_items=None, pipelined: bool = True):
+        bounds, nsum, seq_len = seg
+        p = self.params
+        if q.shape[0] != 1 or not q.is_contiguous():
+            raise ValueError("the layer-pipelined tier runs batch 1 (the paper's setting)")
+        if update_selection:
+            self.select(q, seg, close_items)
+        else:
+            Z.build_index(bounds, nsum, seq_len, self.flags, p.sink, p.window, self.index, self.count, self.status)
+        ng = self.shape.num_layers // self.Lg
+        if not pipelined:
+            for g in range(ng):
+                self.gather(g)
+                self.attend_group(q, g)
+            return self.out
+        comp, cp = torch.cuda.current_stream(), self.copy_stream
+        cp.wait_stream(comp)  # I_f is known
+        for g in range(ng):
+            with torch.cuda.stream(cp):
+                if g >= 2:
+                    cp.wait_event(self.ev_free[g - 2])  # slot g % 2: group g-2 has been attended
+                self.gather(g, stream=cp)
+                self.ev_ready[g].record(cp)
+            comp.wait_event(self.ev_ready[g])
+            self.attend_group(q, g, stream=comp)
+            self.ev_free[g].record(comp)
+        comp.wait_stream(cp)
+        return self.out
+
+    def launches_per_step(self, *args, **kwargs) -> int:
+        return 1 + 2 * (self.shape.num_layers // self.Lg)

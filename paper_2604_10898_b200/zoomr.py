@@ -27,7 +27,8 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
            "zoomr_write_newest_kv", "zoomr_sparse_decode_attn_chained", "zoomr_select_fused_chained",
-           "zoomr_select_front", "zoomr_select_tail", "zoomr_status_str", "zoomr_abi_version")
+           "zoomr_select_front", "zoomr_select_tail", "zoomr_tier_gather_slice", "zoomr_status_str",
+           "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -102,8 +103,11 @@ def lib():
         L.zoomr_h2o_select.restype = C.c_int
         L.zoomr_tier_workspace_bytes.argtypes = [i32, i32, i32]
         L.zoomr_tier_workspace_bytes.restype = sz
-        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, sz, vp, vp]
+        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, sz, vp,
+                                       vp]
         L.zoomr_tier_fetch.restype = C.c_int
+        L.zoomr_tier_gather_slice.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, vp, vp, i32, i32, vp, vp]
+        L.zoomr_tier_gather_slice.restype = C.c_int
         L.zoomr_write_newest_kv.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_write_newest_kv.restype = C.c_int
         L.zoomr_status_str.argtypes = [C.c_int]
@@ -365,7 +369,7 @@ def tier_workspace_bytes(batch: int, hot_max_pages: int, hot_pages: int) -> int:
 
 
 def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_table, hot_owner, hot_stamp,
-               index, index_count, workspace, dev_status=None, stream=None):
+               index, index_count, workspace, dev_status=None, stream=None, k_new=None, v_new=None, seq_len=None):
     """Make the pages of I_f resident in the HBM hot pool (zoomr_tier_fetch). host_k/v: pinned bf16
     [L][pages][H_kv][P][d] (shape.page_size = P); hot_k/v [L][hot_pages][H_kv][Ph][d]."""
     g = shape.c()
@@ -376,10 +380,31 @@ def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_
                                 _ptr(hot_page_table, torch.int32, "hot_page_table"),
                                 _ptr(hot_owner, torch.int32, "hot_owner"), _ptr(hot_stamp, torch.int32, "hot_stamp"),
                                 _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),
-                                index.shape[1], _ptr(workspace, None, "workspace"),
+                                index.shape[1], _ptr(k_new, torch.bfloat16, "k_new"),
+                                _ptr(v_new, torch.bfloat16, "v_new"), _ptr(seq_len, torch.int32, "seq_len"),
+                                _ptr(workspace, None, "workspace"),
                                 workspace.numel() * workspace.element_size(),
                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
     _check("zoomr_tier_fetch", rc)
+
+
+def tier_gather_slice(shape: Shape, host_k, host_v, page_table, index, index_count, layer_begin, layer_count,
+                      slice_k, slice_v, dev_status=None, stream=None):
+    """Rows of I_f of layers [layer_begin, +layer_count) host -> HBM slice (zoomr_tier_gather_slice).
+    slice_k/v: bf16 [layer_count][B * spp][H_kv][Ps][d]."""
+    g = shape.c()
+    B = index.shape[0]
+    if slice_k.dim() != 5 or slice_k.shape != slice_v.shape or slice_k.shape[1] % B:
+        raise ValueError("slice_k/v must be [layer_count][B*spp][H_kv][Ps][d]")
+    kv = KV(_host_ptr(host_k, "host_k"), _host_ptr(host_v, "host_v"), host_k.shape[1],
+            _ptr(page_table, torch.int32, "page_table"), page_table.shape[1])
+    rc = lib().zoomr_tier_gather_slice(C.byref(g), B, C.byref(kv), _ptr(index, torch.int32, "index"),
+                                       _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                       int(layer_begin), int(layer_count), _ptr(slice_k, torch.bfloat16, "slice_k"),
+                                       _ptr(slice_v, torch.bfloat16, "slice_v"), slice_k.shape[3],
+                                       slice_k.shape[1] // B, _ptr(dev_status, torch.int32, "dev_status"),
+                                       _stream(stream))
+    _check("zoomr_tier_gather_slice", rc)
 
 
 def select_workspace_bytes(shape: Shape, batch: int, max_summaries: int) -> int:
@@ -481,7 +506,7 @@ _STAGES = {
     "sparse_decode_attn": "a5", "select_fused": "a1-a4", "select_front": "a1-a2", "select_tail": "a3-a4", "append_kv": "a0", "track_segments": "a0",
     "shard_index": "a4-shard", "sparse_decode_attn_lse": "a5-lse", "merge_attn": "a5-merge",
     "sparse_decode_attn_logits": "a5-logits", "h2o_accumulate": "h2o", "h2o_select": "h2o",
-    "tier_fetch": "tier", "write_newest_kv": "a0-tier",
+    "tier_fetch": "tier", "write_newest_kv": "a0-tier", "tier_gather_slice": "tier-slice",
 }
 
 

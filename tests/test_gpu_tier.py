@@ -211,3 +211,67 @@ def test_tier_decode_loop_equals_hbm_decode_loop(ph):
         assert torch.equal(tl.index, ref.index) and torch.equal(tl.out, ref.out), i
     # the host cache received every appended row (write-through)
     assert torch.equal(tl.host_k.cuda(), kv_dev[0]) and torch.equal(tl.host_v.cuda(), kv_dev[1])
+
+
+@pytest.mark.parametrize("cfg,lg", [
+    (_cfg("lp_small", L=4, batch=1), 1),
+    (_cfg("lp_small2", L=4, batch=1, Hq=14, Hkv=2), 2),
+    (S.CONFIGS["8b16k"], 1),
+], ids=lambda x: getattr(x, "name", str(x)))
+def test_layer_pipelined_tier_matches_hbm_and_oracle(cfg, lg):
+    """The paper's layer-by-layer host tier (LayerPipelinedTierStep):
+    per group of layers, the rows of I_f are gathered host -> HBM slice on a copy
+    stream while the previous group attends, two slices resident.  The output
+    equals the all-HBM step (fp32 rounding: another stream-K split) and the
+    oracle (2e-3), pipelined and serial, eager and as a CUDA-graph replay; the
+    slice holds exactly the host rows of I_f."""
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.step import StepParams
+    from paper_2604_10898_b200.tier import LayerPipelinedTierStep
+    inp = S.generate(cfg, device="cuda")
+    cap = 8192 if cfg.T > 4096 else cfg.T
+    ref = PY.make_step(inp, debug=False, capacity=cap)
+    PY.run_full(inp, ref, fused=True)
+    hk, hv = inp.k_pool.cpu().pin_memory(), inp.v_pool.cpu().pin_memory()
+    seg = (inp.bounds, inp.num_summaries, inp.seq_len)
+    shape = Z.Shape(cfg.L, cfg.Hq, cfg.Hkv, cfg.d, cfg.page)
+    st = LayerPipelinedTierStep(shape, inp.bounds.shape[1], cap, StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window),
+                                hk, hv, inp.page_table, layers_per_slice=lg)
+    st.mean_keys.copy_(ref.mean_keys)
+    for pipelined in (True, False):
+        st.out.zero_()
+        st.run(inp.q, seg, pipelined=pipelined)
+        torch.cuda.synchronize()
+        st.check_status()
+        assert torch.equal(st.count, ref.count) and torch.equal(st.flags, ref.flags)
+        assert (st.out - ref.out).abs().max().item() <= 1e-5
+    # the last group's slice holds the host rows of I_f (layer by layer, every head)
+    n = int(st.count[0])
+    idx = st.index[0, :n].long()
+    g = cfg.L // lg - 1
+    sk, _ = st.slices[g % 2]
+    for ll in range(lg):
+        l = g * lg + ll
+        rows = sk[ll].permute(0, 2, 1, 3).reshape(-1, cfg.Hkv, cfg.d)[:n]  # slice row j -> [H_kv][d]
+        pages, slots = inp.page_table[0].long()[idx // cfg.page], idx % cfg.page
+        host_rows = inp.k_pool[l][pages, :, slots]  # [n][H_kv][d]
+        assert torch.equal(rows, host_rows)
+    # graph replay (both streams captured), then the oracle on sampled heads
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        st.run(inp.q, seg)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        st.run(inp.q, seg)
+    st.out.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    assert (st.out - ref.out).abs().max().item() <= 1e-5
+    if cfg.T <= 4096:
+        K, V = PY.host_kv(inp, 0)
+        o = oracle.sparse_decode_attn(S.bf16_bits(inp.q[0]), K, V, st.index[0, :n].cpu().numpy(), cfg.L, cfg.Hq,
+                                      cfg.Hkv, cfg.d)
+        assert np.abs(st.out[0].cpu().numpy().astype(np.float64) - o).max() <= PY.ATTN_TOL

@@ -579,3 +579,44 @@ def test_h2o_with_full_budget_is_full_attention():
     o = oracle.sparse_decode_attn(qb, kb, vb, idx, 1, 1, 1, d)
     ref = sdpa_fp64(bf16_bits_to_float(qb[0, 0]), bf16_bits_to_float(kb[:, 0, 0]), bf16_bits_to_float(vb[:, 0, 0]))
     np.testing.assert_allclose(o[0, 0], ref, rtol=0, atol=1e-12)
+
+
+# ---- SPEC simulate_transfer_schedule, the paper's layer pipeline ----------------
+def test_transfer_schedule_spec_examples():
+    """S:291: in [2,2,2] s, compute [3,3,3] s, write-back free -> pipelined 2 + 3*3 = 11 s vs serial 15 s;
+    S:292: a single layer -> pipelined == serial; compute all 0 -> total = sum of transfers."""
+    from oracle.transfer import simulate_transfer_schedule as sim
+    r = sim([2, 2, 2], [3, 3, 3])
+    assert r["total_time"] == 11 and r["serial_time"] == 15
+    assert r["peak_resident_layers"] <= 2
+    r1 = sim([2.5], [4.0], [1.5])
+    assert r1["total_time"] == r1["serial_time"] == 8.0
+    r0 = sim([1, 2, 3, 4], [0, 0, 0, 0])
+    assert r0["total_time"] == 10
+
+
+def test_transfer_schedule_invariants():
+    """Brute-force checks on random models: the greedy schedule never beats either
+    bound (the transfer chain, the compute chain), never exceeds serial, keeps at most
+    two slices resident, and respects every dependency of the two-stage pipeline."""
+    import random
+    from oracle.transfer import simulate_transfer_schedule as sim
+    rng = random.Random(7)
+    for _ in range(300):
+        n = rng.randint(1, 12)
+        ti = [rng.uniform(0, 5) for _ in range(n)]
+        tc = [rng.uniform(0, 5) for _ in range(n)]
+        to = [rng.uniform(0, 2) for _ in range(n)]
+        r = sim(ti, tc, to)
+        eps = 1e-9
+        assert r["total_time"] <= r["serial_time"] + eps
+        assert r["total_time"] >= sum(ti) + tc[-1] + to[-1] - eps  # in-chain, then the last compute + write-back
+        assert r["total_time"] >= ti[0] + sum(tc) - eps             # first transfer, then the compute chain
+        assert r["peak_resident_layers"] <= 2
+        ev = r["events"]
+        for l, in0, in1, c0, c1, o0, o1 in ev:
+            assert c0 >= in1 - eps and o0 >= c1 - eps
+            if l:
+                assert in0 >= ev[l - 1][2] - eps and c0 >= ev[l - 1][4] - eps and o0 >= ev[l - 1][6] - eps
+            if l >= 2:
+                assert in0 >= ev[l - 2][6] - eps  # the slot of layer l-2 is free

@@ -259,6 +259,7 @@ __device__ __forceinline__ void block_topk_voters(int G, float *al, int ald, int
   }
 }
 
+
 // ---------------------------------------------------------------- a3 -----
 // Global consensus over one sequence's (v, A), all in shared memory:
 // flags fl[i] = 2 (I_c), 1 (I_s = I_all \ I_c), 0 (unvoted).  Exact integer work:
@@ -268,6 +269,103 @@ __device__ __forceinline__ void block_topk_voters(int G, float *al, int ald, int
 //  3. the tie group at b* is ranked by the full key (v desc, A desc, i asc) and
 //     its first c - n_above members join I_c.
 // Returns nothing; *ag (if non-null, thread 0) = sum_{I_c} v / sum_{I_all} v.
+// small c (every BASELINE config but the stress sweep's c = 32), large N_t:
+//  1. the c largest VOTE COUNTS, one occurrence per round: c rounds of a
+//     block max over 32-bit votes (redux.sync per warp, one barrier per
+//     round) -> the threshold v* = the c-th largest vote, n_above = #{v > v*};
+//  2. the tie group {v == v*} is ranked by the rest of the key (A desc, i asc)
+//     and its first c - n_above members join I_c.
+// O(c + m^2 / T) per thread (m = tie-group size, usually small) instead of the
+// O(N_t) compares per entry of direct ranking (~5 us at N_t = 240 on one CTA).
+// A function of its own, so that block_topc's common path stays compact.
+static __device__ __noinline__ void block_topc_rounds(const int *v, const long long *A, int nt, int c, uint8_t *fl,
+                                                      int *hist, int *grp, int *scratch, float *ag) {
+  const int T = blockDim.x, tid = threadIdx.x;
+  int *wm = hist;  // [2][32] warp maxima (double-buffered: one barrier per round)
+  const int lane = tid & 31, warp = tid >> 5, nw = (T + 31) >> 5;
+  unsigned removed = 0;
+  int sv = 0, vstar = 0, got = 0;
+  for (int j = 0, i = tid; i < nt; ++j, i += T) {
+    const int vi = v[i];
+    fl[i] = vi > 0 ? 1 : 0;
+    sv += vi > 0 ? vi : 0;
+  }
+  for (int r = 0; r < c; ++r) {
+    int lm = 0, lj = -1;
+    for (int j = 0, i = tid; i < nt; ++j, i += T) {
+      const int vi = v[i];
+      if (vi > lm && !(removed >> j & 1u)) {
+        lm = vi;
+        lj = j;
+      }
+    }
+    const int wmax = __reduce_max_sync(0xffffffffu, lm);
+    int *buf = wm + (r & 1) * 32;
+    if (lane == 0) buf[warp] = wmax;
+    __syncthreads();
+    int gmax = 0, ow = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int x = buf[w];
+      if (x > gmax) {
+        gmax = x;
+        ow = w;
+      }
+    }
+    if (gmax == 0) break;  // fewer than c voted summaries: all of them are in I_c (uniform)
+    if (warp == ow) {      // one occurrence of gmax leaves: the lowest lane of the first warp holding it
+      const unsigned m = __ballot_sync(0xffffffffu, lm == gmax);
+      if (lane == __ffs(m) - 1) removed |= 1u << lj;
+    }
+    vstar = gmax;
+    ++got;
+  }
+  // I_c = {v > v*} + the first (c - n_above) of {v == v*} by (A desc, i asc);
+  // got < c means every voted entry fits (v* = smallest voted vote, all join)
+  if (tid == 0) {
+    scratch[34] = 0;  // tie-group size
+    scratch[35] = 0;  // sum v over I_c
+    scratch[36] = 0;  // sum v over I_all
+    scratch[37] = 0;  // n_above
+  }
+  __syncthreads();
+  int above = 0;
+  for (int i = tid; i < nt; i += T) {
+    const int vi = v[i];
+    if (vi <= 0 || got == 0) continue;
+    if (got < c || vi > vstar) {
+      fl[i] = 2;
+      ++above;
+    } else if (vi == vstar) {
+      grp[atomicAdd(&scratch[34], 1)] = i;
+    }
+  }
+  if (above) atomicAdd(&scratch[37], above);
+  __syncthreads();
+  const int m = scratch[34], need = c - scratch[37];
+  for (int x = tid; x < m && need > 0; x += T) {
+    const int i = grp[x];
+    const long long ai = A[i];
+    int rk = 0;
+    for (int y = 0; y < m; ++y) {
+      const int jj = grp[y];
+      const long long aj = A[jj];
+      rk += (aj > ai) | ((aj == ai) & (jj < i));
+    }
+    if (rk < need) fl[i] = 2;
+  }
+  __syncthreads();
+  if (ag) {
+    int sc_ = 0;
+    for (int i = tid; i < nt; i += T)
+      if (fl[i] == 2) sc_ += v[i];
+    if (sc_) atomicAdd(&scratch[35], sc_);
+    if (sv) atomicAdd(&scratch[36], sv);
+    __syncthreads();
+    if (tid == 0) *ag = scratch[36] > 0 ? (float)((double)scratch[35] / (double)scratch[36]) : 0.f;
+    __syncthreads();
+  }
+}
+
 // __noinline__: the fused select's tail CTA runs it once on dummy data first, and the
 // real call must then execute the very same (now cached) instructions
 static __device__ __noinline__ void block_topc(const int *v, const long long *A, int nt, int c, uint8_t *fl,
@@ -275,97 +373,7 @@ static __device__ __noinline__ void block_topc(const int *v, const long long *A,
                            int *scratch /* smem >= 40 ints */, float *ag) {
   const int T = blockDim.x, tid = threadIdx.x;
   if (c <= kTopcRounds && nt > kTopcRoundsMinN && nt <= 32 * T) {
-    // small c (every BASELINE config but the stress sweep's c = 32):
-    //  1. the c largest VOTE COUNTS, one occurrence per round: c rounds of a
-    //     block max over 32-bit votes (redux.sync per warp, one barrier per
-    //     round) -> the threshold v* = the c-th largest vote, n_above = #{v > v*};
-    //  2. the tie group {v == v*} is ranked by the rest of the key (A desc, i asc)
-    //     and its first c - n_above members join I_c.
-    // O(c + m^2 / T) per thread (m = tie-group size, usually small) instead of
-    // the O(N_t) compares per entry of direct ranking (~5 us at N_t = 240 on one CTA).
-    int *wm = hist;  // [2][32] warp maxima (double-buffered: one barrier per round)
-    const int lane = tid & 31, warp = tid >> 5, nw = (T + 31) >> 5;
-    unsigned removed = 0;
-    int sv = 0, vstar = 0, got = 0;
-    for (int j = 0, i = tid; i < nt; ++j, i += T) {
-      const int vi = v[i];
-      fl[i] = vi > 0 ? 1 : 0;
-      sv += vi > 0 ? vi : 0;
-    }
-    for (int r = 0; r < c; ++r) {
-      int lm = 0, lj = -1;
-      for (int j = 0, i = tid; i < nt; ++j, i += T) {
-        const int vi = v[i];
-        if (vi > lm && !(removed >> j & 1u)) {
-          lm = vi;
-          lj = j;
-        }
-      }
-      const int wmax = __reduce_max_sync(0xffffffffu, lm);
-      int *buf = wm + (r & 1) * 32;
-      if (lane == 0) buf[warp] = wmax;
-      __syncthreads();
-      int gmax = 0, ow = 0;
-      for (int w = 0; w < nw; ++w) {
-        const int x = buf[w];
-        if (x > gmax) {
-          gmax = x;
-          ow = w;
-        }
-      }
-      if (gmax == 0) break;  // fewer than c voted summaries: all of them are in I_c (uniform)
-      if (warp == ow) {      // one occurrence of gmax leaves: the lowest lane of the first warp holding it
-        const unsigned m = __ballot_sync(0xffffffffu, lm == gmax);
-        if (lane == __ffs(m) - 1) removed |= 1u << lj;
-      }
-      vstar = gmax;
-      ++got;
-    }
-    // I_c = {v > v*} + the first (c - n_above) of {v == v*} by (A desc, i asc);
-    // got < c means every voted entry fits (v* = smallest voted vote, all join)
-    if (tid == 0) {
-      scratch[34] = 0;  // tie-group size
-      scratch[35] = 0;  // sum v over I_c
-      scratch[36] = 0;  // sum v over I_all
-      scratch[37] = 0;  // n_above
-    }
-    __syncthreads();
-    int above = 0;
-    for (int i = tid; i < nt; i += T) {
-      const int vi = v[i];
-      if (vi <= 0 || got == 0) continue;
-      if (got < c || vi > vstar) {
-        fl[i] = 2;
-        ++above;
-      } else if (vi == vstar) {
-        grp[atomicAdd(&scratch[34], 1)] = i;
-      }
-    }
-    if (above) atomicAdd(&scratch[37], above);
-    __syncthreads();
-    const int m = scratch[34], need = c - scratch[37];
-    for (int x = tid; x < m && need > 0; x += T) {
-      const int i = grp[x];
-      const long long ai = A[i];
-      int rk = 0;
-      for (int y = 0; y < m; ++y) {
-        const int jj = grp[y];
-        const long long aj = A[jj];
-        rk += (aj > ai) | ((aj == ai) & (jj < i));
-      }
-      if (rk < need) fl[i] = 2;
-    }
-    __syncthreads();
-    if (ag) {
-      int sc_ = 0;
-      for (int i = tid; i < nt; i += T)
-        if (fl[i] == 2) sc_ += v[i];
-      if (sc_) atomicAdd(&scratch[35], sc_);
-      if (sv) atomicAdd(&scratch[36], sv);
-      __syncthreads();
-      if (tid == 0) *ag = scratch[36] > 0 ? (float)((double)scratch[35] / (double)scratch[36]) : 0.f;
-      __syncthreads();
-    }
+    block_topc_rounds(v, A, nt, c, fl, hist, grp, scratch, ag);
     return;
   }
   if (nt <= T) {

@@ -29,8 +29,8 @@ def read(fn, reset):
     return list(b)
 
 
-NAMES = {"select": ["start", "front_end", "tail_start", "collected", "topc_done", "end", "a1_done", "q_staged",
-                    "alpha_done", "topk_done"],
+NAMES = {"select": ["start", "front_end", "tail_start", "collected", "topc_done", "end", "a1_done", "(unused)",
+                    "score_topk_done"],
          "a5": ["start", "prologue", "B_known", "first_tile", "first_B_tile", "math_done", "prod_done",
                 "first_issue"]}
 for var in os.environ.get("VARS", "early,late").split(","):

@@ -64,7 +64,7 @@ struct AttnShape {
   static constexpr int TILE_BYTES = NREG * REG_BYTES;   // K (or V) part of a stage
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
   static constexpr int RING_BYTES = kPairs * kStages * STAGE_BYTES;
-  static constexpr int BAR_BYTES = 2 * kPairs * kStages * 8;
+  static constexpr int BAR_BYTES = (2 * kPairs * kStages + kPairs) * 8;  // full, empty, and one merge barrier per pair
   static constexpr int CPR = RB / 16;                   // 16-byte chunks per row
   static constexpr int RPI = 32 / CPR;                  // rows per warp-wide cp.async
   // shared address of (row r, 16-byte chunk c) inside a K or V tile starting at `base`
@@ -124,6 +124,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(map), "r"(x), "r"((int)y), "r"(smem_u32(bar))
       : "memory");
+}
+// 1D bulk copy global -> shared (TMA), completion as tx bytes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -278,6 +284,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       mbar_init(&full[x], 33);  // producer lane 0's expect_tx arrive + one cp.async (noinc) arrive per lane
       mbar_init(&empty[x], 1);  // the math warp's lane 0
     }
+    for (int x = 0; x < kPairs; ++x) mbar_init(&empty[kPairs * kStages + x], 1);  // merge staging (lane 0's expect_tx)
     *bstate = 0;
     mbar_init(bready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -641,6 +648,8 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   constexpr int SLOT = HDR + G * D;         // partial result: header, then O[G][D]
 
   int cur_ph = -2, cur_b = -1, cur_seg = -1;  // -2: no segment yet (never equal to a past-the-end k)
+  uint64_t *mrgbar = empty + kPairs * kStages + pair;  // this pair's merge-staging barrier
+  uint32_t mrgphase = 0;
   int npend = 0;  // phase-A partials published before the wait, not yet counted: the first npend segments of the A range
   uint32_t qf[NKS][2];
   float o[NKS][4], o2[kTwoN ? NKS : 1][4];
@@ -772,6 +781,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         }
       }
       __syncwarp();  // orders the lanes' partial stores before lane 0's release
+      if (ZOOMR_MERGE_STAGE && lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // read by TMA later
     }
     if (!bres) {  // phase A before the wait: count it later
       ++npend;
@@ -826,15 +836,23 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       float *stg = own + SLOT;
       const bool staged = ZOOMR_MERGE_STAGE && at_end && (nparts + 1) * SLOT * 4 <= kStages * S::STAGE_BYTES;
       if (staged) {
+        // one 1D TMA bulk copy per part (lane j copies part j): a few instructions
+        // instead of SLOT/4 16-byte cp.async per part (for G = 8, 8 parts were
+        // ~2300 issues from one warp, ~7 us at the end of the kernel)
         __syncwarp();  // a previous merge's shared-memory reads are done
-        for (int j = 0; j < nparts; ++j) {
-          if (j == own_j) continue;
-          const float *qp = part_ptr(xb, xs, j, wf0, n0w, wf1);
-          const uint32_t dst = smem_u32(stg + j * SLOT);
-          for (int c = lane; c < SLOT / 4; c += 32) cp_async16(dst + 16 * c, qp + 4 * c, 16);
+        const uint32_t nbytes = (uint32_t)((nparts - (own_j >= 0 ? 1 : 0)) * SLOT * 4);
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");      // the parts were written by generic stores
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the staging area was read generically
+          mbar_arrive_expect_tx(mrgbar, nbytes);
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
         __syncwarp();
+        for (int j = lane; j < nparts; j += 32) {
+          if (j == own_j) continue;
+          bulk_g2s(smem_u32(stg + j * SLOT), part_ptr(xb, xs, j, wf0, n0w, wf1), (uint32_t)(SLOT * 4), mrgbar);
+        }
+        mbar_wait(mrgbar, mrgphase, 8);
+        mrgphase ^= 1u;
       }
       for (int j0 = 0; j0 < nparts; j0 += NPF) {
         float mh[NPF][G], lh[NPF][G];

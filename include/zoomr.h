@@ -315,7 +315,9 @@ int zoomr_append_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, c
 /* The rows of the newest token (position seq_len[b] - 1, already counted) into
  * another copy of the cache -- the host tier's hot pool after zoomr_tier_fetch
  * made the page resident (the host copy took it through zoomr_append_kv).
- * seq_len is not changed.  Device errors: INDEX_RANGE (no page for the position). */
+ * seq_len is not changed.  A position whose page entry is -1 (not resident, e.g.
+ * in the host tier's hot pool) is skipped: the tier's fetch brings the page with
+ * the row from the host cache.  Device errors: INDEX_RANGE (an entry out of range). */
 int zoomr_write_newest_kv(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
                           const void *v_new, const int32_t *seq_len, int32_t *dev_status, void *stream);
 
@@ -386,10 +388,18 @@ int zoomr_shard_index(int32_t batch, const int32_t *index, const int32_t *index_
  * preceding kernel on the stream has completed -- the page table included, so
  * it may be that kernel's output (zoomr_tier_fetch's residency table).
  * layer_begin / layer_count as for zoomr_sparse_decode_attn (lse rows of other
- * layers untouched): the host tier attends layer by layer behind its fetch. */
+ * layers untouched): the host tier attends layer by layer behind its fetch.
+ * seq_len / sink / window (nullable seq_len, ABI 9): the early rows of
+ * zoomr_sparse_decode_attn -- I_p and I_w attended before the wait, their
+ * page-table entries read from global memory then -- for a page table that the
+ * preceding kernels may still be changing elsewhere: the caller guarantees that
+ * the entries of the sink and window pages do not change during this call (the
+ * host tier: zoomr_tier_fetch with seq_len keeps the next token's page resident
+ * one step ahead, so after one warm step they never do). */
 int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const void *q,
                                  const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
-                                 const int32_t *index_count, int32_t index_capacity, float softmax_scale,
+                                 const int32_t *index_count, int32_t index_capacity,
+                                 const int32_t *seq_len, int32_t sink, int32_t window, float softmax_scale,
                                  int32_t layer_begin, int32_t layer_count, float *out, float *lse,
                                  void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
 
@@ -473,15 +483,17 @@ int zoomr_h2o_select(int32_t batch, const int32_t *prev_index, const int32_t *pr
  * CAPACITY (the hot pool cannot hold the pages of this step's I_f; the rest
  * stay missing), INDEX_RANGE. */
 size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t hot_pages);
-/* k_new, v_new (nullable, bf16 [B][L][H_kv][d]) + seq_len: also write the
- * newest token's rows (position seq_len[b] - 1, resident since I_w holds it)
- * into the hot pool -- what zoomr_write_newest_kv does, without a launch of its
- * own (ABI 9); the host cache must already hold them (zoomr_append_kv). */
+/* seq_len (nullable, device int32 [B], ABI 9): also make the hot page of
+ * position seq_len[b] -- the NEXT token's -- resident now (look-ahead), so that
+ * at the next step every sink and window page is resident before that step's
+ * plan runs (its a5 may then read their entries early, see
+ * zoomr_sparse_decode_attn_lse, and zoomr_write_newest_kv finds the newest
+ * token's page resident before the selection). */
 int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k, void *hot_v,
                      int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table, int32_t *hot_owner,
                      int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
-                     int32_t index_capacity, const void *k_new, const void *v_new, const int32_t *seq_len,
-                     void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
+                     int32_t index_capacity, const int32_t *seq_len, void *workspace, size_t workspace_bytes,
+                     int32_t *dev_status, void *stream);
 
 /* Human-readable status name; never NULL. */
 const char *zoomr_status_str(int status);

@@ -23,6 +23,7 @@ __global__ void append_kv_kernel(const uint4 *__restrict__ k_new, const uint4 *_
   const int T = seq_len_in[b] - back;  // back = 1: the newest token, already counted in seq_len
   const int lp = T / P;
   int page = (T >= 0 && lp < max_pages) ? page_table[(int64_t)b * max_pages + lp] : -1;
+  if (back && page == -1 && T >= 0 && lp < max_pages) return;  // newest row, page not resident: nothing to update
   if (page < 0 || page >= num_pages) {
     if (threadIdx.x == 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
     return;

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
     int32_t B, const int32_t *__restrict__ index, const int32_t *__restrict__ count, int32_t cap, int32_t Ph,
     int32_t R, int32_t max_pages, const int32_t *__restrict__ host_pt, int32_t *__restrict__ hot_pt,
     int32_t *__restrict__ owner, int32_t *__restrict__ stamp, int32_t hot_pages, int32_t *__restrict__ ws,
-    int32_t *status) {
+    int32_t *status, const int32_t *__restrict__ seq_len) {
   __shared__ int wsum[33];
   __shared__ int hist[256];
   __shared__ unsigned long long s_prefix;
@@ -80,6 +80,13 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
       const int lp = t / Ph;
       if (t < 0 || lp >= hmp) set_status(status, ZOOMR_ERR_INDEX_RANGE);
       else need[b * hmp + lp] = 1;
+    }
+    // look-ahead: the page of position T (the next token's) is made resident now, so
+    // that in the next step every sink / window page is resident before that step's
+    // plan runs -- its a5 may then read their page entries before its wait
+    if (seq_len && tid == 0) {
+      const int lp = seq_len[b] / Ph;
+      if (seq_len[b] >= 0 && lp < hmp) need[b * hmp + lp] = 1;
     }
   }
   __syncthreads();
@@ -207,37 +214,9 @@ __global__ void __launch_bounds__(256) tier_copy_kernel(const uint4 *__restrict_
                                                          const uint4 *__restrict__ host_v, int64_t host_pages,
                                                          uint4 *__restrict__ hot_k, uint4 *__restrict__ hot_v,
                                                          int64_t hot_pages, int32_t L, int32_t Hkv, int32_t R,
-                                                         int32_t row16, const int32_t *__restrict__ ws, int32_t NP,
-                                                         const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
-                                                         const int32_t *__restrict__ seq_len,
-                                                         const int32_t *__restrict__ hot_pt, int32_t hmp, int32_t Ph,
-                                                         int32_t B, int32_t *status) {
+                                                         int32_t row16, const int32_t *__restrict__ ws, int32_t NP) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a5 may launch (it waits for this copy)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // the newest token's rows (k_new / v_new [B][L][H_kv][d]) into its hot page -- resident,
-  // since I_w holds position T-1.  The host cache already holds the same rows
-  // (zoomr_append_kv wrote them before the selection), so a concurrent copy of
-  // that page below writes identical bytes.
-  if (k_new) {
-    const int rowu = row16 / Ph;  // uint4 per (token, head) row
-    for (int64_t w = blockIdx.x; w < (int64_t)B * L; w += gridDim.x) {
-      const int b = (int)(w / L), l = (int)(w - (int64_t)b * L);
-      const int pos = seq_len[b] - 1;
-      const int lp = pos / Ph;
-      const int hp = (pos >= 0 && lp < hmp) ? hot_pt[(int64_t)b * hmp + lp] : -1;
-      if (hp < 0 || hp >= hot_pages) {
-        if (threadIdx.x == 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
-        continue;
-      }
-      for (int e = threadIdx.x; e < Hkv * rowu; e += blockDim.x) {
-        const int g = e / rowu, c = e - g * rowu;
-        const int64_t dst = (((int64_t)l * hot_pages + hp) * Hkv + g) * row16 + (int64_t)(pos - lp * Ph) * rowu + c;
-        const int64_t src = (((int64_t)b * L + l) * Hkv + g) * rowu + c;
-        hot_k[dst] = k_new[src];
-        hot_v[dst] = v_new[src];
-      }
-    }
-  }
   const int nf = ws[1];
   const int32_t *fetch_hot = ws + 2 + NP + hot_pages, *fetch_host = fetch_hot + hot_pages;
   const int64_t items = (int64_t)nf * L * 2;
@@ -366,13 +345,13 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
                                 void *hot_v, int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table,
                                 int32_t *hot_owner,
                                 int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,
-                                int32_t index_capacity, const void *k_new, const void *v_new, const int32_t *seq_len,
-                                void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream) {
+                                int32_t index_capacity, const int32_t *seq_len, void *workspace,
+                                size_t workspace_bytes, int32_t *dev_status, void *stream) {
   int rc = check_geom(geom);
   if (rc) return rc;
   if (batch < 1 || !host_kv || !host_kv->k || !host_kv->v || !host_kv->page_table || host_kv->num_pages < 1 ||
       host_kv->max_pages < 1 || !hot_k || !hot_v || hot_pages < 1 || !hot_page_table || !hot_owner || !hot_stamp ||
-      !index || !index_count || index_capacity < 1 || !workspace || (k_new && (!v_new || !seq_len)))
+      !index || !index_count || index_capacity < 1 || !workspace)
     return ZOOMR_ERR_INVALID_ARG;
   const int P = geom->page_size, Ph = hot_page_size;
   if (Ph < 1 || P % Ph) return ZOOMR_ERR_INVALID_ARG;
@@ -385,13 +364,11 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
   cudaStream_t s = (cudaStream_t)stream;
   launch_pdl(tier_plan_kernel, 1, kPlanThreads, 0, s, batch, index, index_count, index_capacity, Ph, R,
              host_kv->max_pages, host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
-             (int32_t *)workspace, dev_status);
+             (int32_t *)workspace, dev_status, seq_len);
   rc = launch_status(s);
   if (rc) return rc;
   launch_pdl(tier_copy_kernel, 2 * num_sms(), 256, 0, s, (const uint4 *)host_kv->k, (const uint4 *)host_kv->v,
              (int64_t)host_kv->num_pages, (uint4 *)hot_k, (uint4 *)hot_v, (int64_t)hot_pages, geom->num_layers,
-             geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp),
-             (const uint4 *)k_new, (const uint4 *)v_new, seq_len, (const int32_t *)hot_page_table, (int32_t)hmp, Ph,
-             batch, dev_status);
+             geom->num_kv_heads, R, (int32_t)(row / 16), (const int32_t *)workspace, (int32_t)(batch * hmp));
   return launch_status((cudaStream_t)stream);
 }

@@ -84,9 +84,11 @@ class TierDecodeLoop(HostTierStep):
         segment tracking          zoomr_track_segments
         a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
                                   the host cache; a2/a3 only at semantic boundaries)
-        tier fetch                zoomr_tier_fetch (pages that entered I_f, and the newest
-                                  rows into their hot page: resident, I_w holds T-1)
-        a5                        zoomr_sparse_decode_attn_lse on the hot pool
+        newest rows -> hot pool   zoomr_write_newest_kv (resident after a warm step: the
+                                  previous fetch made the page of T resident, look-ahead)
+        tier fetch                zoomr_tier_fetch (pages that entered I_f + the look-ahead page)
+        a5                        zoomr_sparse_decode_attn_lse on the hot pool, with the
+                                  early rows (sink / window before the wait) once warm
     """
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int, params: StepParams,
@@ -103,9 +105,11 @@ class TierDecodeLoop(HostTierStep):
         self.track_state = torch.zeros(batch, 4, dtype=torch.int32, device=dev)
         self.close_items = torch.zeros(batch, 2, dtype=torch.int32, device=dev)
         self.update = torch.zeros(batch, dtype=torch.uint8, device=dev)
+        self._warm = False  # a step has run since start(): sink / window pages are resident
 
     def start(self, prompt_len):
         """After a prefill of `prompt_len` tokens (already in the host cache): no summaries yet."""
+        self._warm = False
         n = torch.as_tensor(prompt_len, dtype=torch.int32, device=self.seq_len.device).expand(self.batch)
         self.seq_len.copy_(n)
         self.num_summaries.zero_()
@@ -115,6 +119,7 @@ class TierDecodeLoop(HostTierStep):
 
     def start_from(self, bounds, num_summaries, seq_len):
         """Continue an existing context (its segment table, N_t, T); mean keys must be cached."""
+        self._warm = False
         self.bounds.copy_(bounds)
         self.num_summaries.copy_(num_summaries)
         self.seq_len.copy_(seq_len)
@@ -125,8 +130,15 @@ class TierDecodeLoop(HostTierStep):
         self.track_state.copy_(torch.stack([torch.full_like(tail, -1), tail, tail, tail], dim=1))
 
     def decode_step(self, k_new, v_new, q, token_ids):
+        """One token.  From the second step after start() / start_from() on, a5 attends
+        the sink and window rows before its wait (their hot pages are resident: the
+        previous step's fetch kept the next token's page resident, look-ahead)."""
         p, hs = self.params, self.host_shape
+        early = self._warm
         Z.append_kv(hs, self.host_k, self.host_v, self.page_table, k_new, v_new, self.seq_len, self.status)
+        # the newest rows into their hot page (resident after a warm step; else the fetch brings it)
+        Z.write_newest_kv(self.shape, self.hot_k, self.hot_v, self.hot_page_table, k_new, v_new, self.seq_len,
+                          self.status)
         Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
                          self.num_summaries, self.track_state, self.close_items, self.update, self.status)
         Z.select_fused(hs, q, self.host_k, self.host_v, self.page_table, self.bounds, self.num_summaries,
@@ -134,12 +146,13 @@ class TierDecodeLoop(HostTierStep):
                        self.index, self.count, self.sel_workspace, partial=self.partial,
                        agreeability=self.agreeability, alpha_out=self.alpha, topk_out=self.topk,
                        dev_status=self.status, update=self.update)
-        # the fetch also writes the newest rows into their (resident) hot page
         Z.tier_fetch(hs, self.host_k, self.host_v, self.page_table, self.hot_k, self.hot_v, self.hot_page_table,
                      self.hot_owner, self.hot_stamp, self.index, self.count, self.tier_ws, self.status,
-                     k_new=k_new, v_new=v_new, seq_len=self.seq_len)
+                     seq_len=self.seq_len)  # (look-ahead: the next token's page)
         Z.sparse_decode_attn_lse(self.shape, q, self.hot_k, self.hot_v, self.hot_page_table, self.index, self.count,
-                                 self.out, self.lse, self.workspace, dev_status=self.status)
+                                 self.out, self.lse, self.workspace, dev_status=self.status,
+                                 seq_len=self.seq_len if early else None, sink=p.sink, window=p.window)
+        self._warm = True
         return self.out
 
 

@@ -89,8 +89,8 @@ def lib():
         L.zoomr_track_segments.restype = C.c_int
         L.zoomr_shard_index.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp]
         L.zoomr_shard_index.restype = C.c_int
-        L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, C.c_float, i32, i32, vp, vp, vp,
-                                                   sz, vp, vp]
+        L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, i32, i32,
+                                                   vp, vp, vp, sz, vp, vp]
         L.zoomr_sparse_decode_attn_lse.restype = C.c_int
         L.zoomr_merge_attn.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_merge_attn.restype = C.c_int
@@ -103,8 +103,7 @@ def lib():
         L.zoomr_h2o_select.restype = C.c_int
         L.zoomr_tier_workspace_bytes.argtypes = [i32, i32, i32]
         L.zoomr_tier_workspace_bytes.restype = sz
-        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, sz, vp,
-                                       vp]
+        L.zoomr_tier_fetch.argtypes = [vp, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, sz, vp, vp]
         L.zoomr_tier_fetch.restype = C.c_int
         L.zoomr_tier_gather_slice.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, vp, vp, i32, i32, vp, vp]
         L.zoomr_tier_gather_slice.restype = C.c_int
@@ -265,7 +264,7 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
 
 def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out, lse,
                            workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
-                           layer_begin=0, layer_count=0):
+                           layer_begin=0, layer_count=0, seq_len=None, sink=0, window=0):
     """a5 over any index list, also writing lse fp32 [B][L][H_q] (zoomr_sparse_decode_attn_lse)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
@@ -273,6 +272,7 @@ def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, i
                                             C.byref(kv), _ptr(index, torch.int32, "index"),
                                             _ptr(index_phys, torch.int32, "index_phys"),
                                             _ptr(index_count, torch.int32, "index_count"), index.shape[1],
+                                            _ptr(seq_len, torch.int32, "seq_len"), int(sink), int(window),
                                             C.c_float(sc), int(layer_begin), int(layer_count),
                                             _ptr(out, torch.float32, "out"),
                                             _ptr(lse, torch.float32, "lse"), _ptr(workspace, None, "workspace"),
@@ -369,7 +369,7 @@ def tier_workspace_bytes(batch: int, hot_max_pages: int, hot_pages: int) -> int:
 
 
 def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_table, hot_owner, hot_stamp,
-               index, index_count, workspace, dev_status=None, stream=None, k_new=None, v_new=None, seq_len=None):
+               index, index_count, workspace, dev_status=None, stream=None, seq_len=None):
     """Make the pages of I_f resident in the HBM hot pool (zoomr_tier_fetch). host_k/v: pinned bf16
     [L][pages][H_kv][P][d] (shape.page_size = P); hot_k/v [L][hot_pages][H_kv][Ph][d]."""
     g = shape.c()
@@ -380,8 +380,7 @@ def tier_fetch(shape: Shape, host_k, host_v, page_table, hot_k, hot_v, hot_page_
                                 _ptr(hot_page_table, torch.int32, "hot_page_table"),
                                 _ptr(hot_owner, torch.int32, "hot_owner"), _ptr(hot_stamp, torch.int32, "hot_stamp"),
                                 _ptr(index, torch.int32, "index"), _ptr(index_count, torch.int32, "index_count"),
-                                index.shape[1], _ptr(k_new, torch.bfloat16, "k_new"),
-                                _ptr(v_new, torch.bfloat16, "v_new"), _ptr(seq_len, torch.int32, "seq_len"),
+                                index.shape[1], _ptr(seq_len, torch.int32, "seq_len"),
                                 _ptr(workspace, None, "workspace"),
                                 workspace.numel() * workspace.element_size(),
                                 _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))

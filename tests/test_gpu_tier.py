@@ -152,9 +152,11 @@ def test_tier_pool_too_small_reports_capacity():
 
 @pytest.mark.parametrize("ph", [0, 8])
 def test_tier_decode_loop_equals_hbm_decode_loop(ph):
-    """Algorithm 1's decode loop over the host tier (write-through append, a1 from the host cache,
-    fetch, newest rows into the hot pool) against the all-HBM DecodeLoop on the same token stream:
-    segment table, flags, I_f and outputs identical at every step, eagerly and as graph replays."""
+    """Algorithm 1's decode loop over the host tier (write-through append, newest rows into the
+    hot pool, a1 from the host cache, look-ahead fetch, a5 with early rows once warm) against the
+    all-HBM DecodeLoop on the same token stream: segment table, flags, I_f and outputs identical
+    at every step (outputs bit-identical from the tier's second step on), eagerly and as graph
+    replays."""
     from paper_2604_10898_b200 import zoomr as Z
     from paper_2604_10898_b200.step import DecodeLoop, StepParams
     from paper_2604_10898_b200.tier import TierDecodeLoop
@@ -169,7 +171,9 @@ def test_tier_decode_loop_equals_hbm_decode_loop(ph):
     v_pool = torch.randn(L, B * pages, Hkv, P, d, generator=gen).bfloat16()
     page_table = torch.randperm(B * pages, generator=gen).int().view(B, pages).contiguous().cuda()
     shape = Z.Shape(L, Hq, Hkv, d, P)
-    ref = DecodeLoop(shape, B, MS, T_max, prm, BEGIN, END, BOUNDARY, early_known=False)
+    # both loops attend the sink / window rows before their wait (the tier from its second
+    # step on, once the look-ahead fetch has made the next token's page resident)
+    ref = DecodeLoop(shape, B, MS, T_max, prm, BEGIN, END, BOUNDARY, early_known=True)
     kv_dev = (k_pool.cuda(), v_pool.cuda(), page_table)
     tl = TierDecodeLoop(shape, B, MS, T_max, prm, k_pool.pin_memory(), v_pool.pin_memory(), page_table,
                         hot_pages=B * pages * (P // (ph or P)), begin_id=BEGIN, end_id=END, boundary_ids=BOUNDARY,
@@ -191,7 +195,10 @@ def test_tier_decode_loop_equals_hbm_decode_loop(ph):
         assert torch.equal(tl.seq_len, ref.seq_len) and torch.equal(tl.num_summaries, ref.num_summaries)
         assert torch.equal(tl.bounds, ref.bounds) and torch.equal(tl.flags, ref.flags)
         assert torch.equal(tl.count, ref.count) and torch.equal(tl.index, ref.index)
-        assert torch.equal(tl.out, ref.out), i
+        if i == 0:  # the tier's first step attends index-only (cold hot pool): another split, fp32 rounding
+            assert (tl.out - ref.out).abs().max().item() <= 1e-5
+        else:
+            assert torch.equal(tl.out, ref.out), i
     assert int(tl.num_summaries.min()) >= 1
     # the rest as graph replays (inputs copied into static buffers)
     sk, sv, sq, st_ = kin[0].clone(), vin[0].clone(), qs[0].clone(), toks[0].clone()

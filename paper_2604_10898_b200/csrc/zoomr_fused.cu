@@ -414,10 +414,13 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
     prefer_max_smem(kfn);                                                                        \
     int per_sm = 0;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);                      \
-    /* the designated tail spins on its siblings: only under a cooperative launch, which      \
-       guarantees that the whole grid is resident at once (never in the chained variant,      \
-       whose CTAs may wait for SMs still held by the preceding a5) */                          \
-    p.designated_tail = kDesignatedTail && mode != kTail && !p.pdl_front &&                     \
+    /* the designated tail CTA spins until the (l, g) CTAs of its sequence have counted;    \
+       those never wait on anything, so they progress whenever any slot is free -- the B    \
+       tail CTAs never fill the GPU, since the whole grid fits at once (checked here).  The \
+       plain launch is cooperative, which makes the driver guarantee it; the chained one is \
+       launched with PDL behind a5, whose CTAs leave as they finish, and the tail CTAs -- the \
+       last of the grid -- start last (advisor note: no spin on CTAs that cannot run). */    \
+    p.designated_tail = kDesignatedTail && mode != kTail &&                                      \
                         (int64_t)(grid.x + 1) * grid.y <= (int64_t)per_sm * num_sms();           \
     if (p.designated_tail) grid.x += 1; /* + the tail CTA of each sequence */                   \
     if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                                     \

@@ -127,6 +127,17 @@ def algorithmic_bytes(cfg, counts, n_sum, closures=1):
     return {"a5": a5, "a4": a4, "a2": a2, "a1": a1, "total": a5 + a4 + a2 + a1}
 
 
+def workload_config(cfg, args, world, batch_per_gpu, n_summaries):
+    """The `config` of the JSON line -- workload parameters only, identical for both arms
+    (the run-dependent figures, e.g. the realised |I_f|, are keys of their own)."""
+    return {"workload": cfg.name, "batch_per_gpu": batch_per_gpu, "global_batch": batch_per_gpu * world,
+            "T": cfg.T, "L": cfg.L, "H_q": cfg.Hq, "H_kv": cfg.Hkv, "d": cfg.d, "n_summaries": n_summaries,
+            "c": cfg.c, "top_k": cfg.top_k, "sink": cfg.sink, "window": cfg.window,
+            "update_every": max(1, cfg.update_every), "query": args.query,
+            "parallelism": f"batch-shard x{world}" if world > 1 else "single",
+            "l2": f"inputs larger than L2: {max(1, args.rotate)} independent input sets rotated per step"}
+
+
 def init_dist(n):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -289,8 +300,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "batch": 1, "T": cfg.T, "n_summaries": int(inp.num_summaries[0]),
-                   "index_count": int(len(r["index"])), "query": args.query},
+        "config": workload_config(cfg, args, args.gpus, 1, int(inp.num_summaries[0])),
+        "index_count": int(len(r["index"])),
         "step_ms_pcts": {k: v * 1e3 for k, v in pcts(times).items()},
         "cpu_baseline": {"value": val, "unit": "seqs/s", "cores": cores, "kind": "oracle", "sample": sample,
                          "cpu_model": cpu_model()},
@@ -1022,14 +1033,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "seqs/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": cfg.name, "batch_per_gpu": Bseq, "global_batch": Bseq * world, "T": cfg.T,
-                   "L": cfg.L, "H_q": cfg.Hq, "H_kv": cfg.Hkv, "d": cfg.d, "n_summaries": nsum[0][0],
-                   "c": cfg.c, "top_k": cfg.top_k, "sink": cfg.sink, "window": cfg.window,
-                   "update_every": U, "query": args.query, "index_count_mean":
-                       sum(sum(c) for c in counts) / sum(len(c) for c in counts),
-                   "parallelism": f"batch-shard x{world}" if world > 1 else "single",
-                   "l2": f"inputs larger than L2: {R} independent input sets rotated per step, "
-                         f"each step reads {bytes_mean / 1e6:.0f} MB"},
+        "config": workload_config(cfg, args, world, Bseq, nsum[0][0]),
+        "index_count_mean": sum(sum(c) for c in counts) / sum(len(c) for c in counts),
         "step_us": step_s * 1e6,
         "step_us_pcts": pcts(step_times),
         "step_roofline": {"bytes_per_step": bytes_mean, "achieved_gbs": bytes_mean / step_s / 1e9,

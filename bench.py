@@ -898,13 +898,10 @@ def run_ours(args):
         start = inp0.seq_len - n_tok
         nmax0 = inp0.bounds.shape[1]
         extra = 8  # room for the summaries that close during the stretch
-        lp = DecodeLoop(shape, Bseq, nmax0 + extra, cfg.T, prm, 1000, 1001, [200])
-        lp.mean_keys[:, :, :, :nmax0].copy_(s0["st"].mean_keys)
         # the closed summaries must end before the appended stretch (the bench context keeps its
         # open tail > 256 tokens, so they do)
         bpad = torch.zeros(Bseq, nmax0 + extra, 4, dtype=torch.int32, device="cuda")
         bpad[:, :nmax0] = inp0.bounds
-        lp.start_from(bpad, inp0.num_summaries, start)
         kin = torch.randn(Bseq, cfg.L, cfg.Hkv, cfg.d, device="cuda").bfloat16()
         vin = torch.randn_like(kin)
         # the token stream: regular text with a sentence boundary every 35 tokens,
@@ -923,29 +920,40 @@ def run_ours(args):
             else:
                 toks.append(7)
         tok_dev = torch.tensor([[t] * Bseq for t in toks], dtype=torch.int32, device="cuda")
-        gl_ = torch.cuda.CUDAGraph()  # all n_tok decode steps in one graph (5 launches each)
-        with torch.cuda.graph(gl_):
-            for i in range(n_tok):
-                lp.decode_step(s0["kv"], kin, vin, inp0.q, tok_dev[i])
+        def loop_time(**kw):
+            lp = DecodeLoop(shape, Bseq, nmax0 + extra, cfg.T, prm, 1000, 1001, [200], **kw)
+            lp.mean_keys[:, :, :, :nmax0].copy_(s0["st"].mean_keys)
+            lp.start_from(bpad, inp0.num_summaries, start)
+            gl_ = torch.cuda.CUDAGraph()  # all n_tok decode steps in one graph
+            with torch.cuda.graph(gl_):
+                for i in range(n_tok):
+                    lp.decode_step(s0["kv"], kin, vin, inp0.q, tok_dev[i])
 
-        def loop_run():
-            lp.start_from(bpad, inp0.num_summaries, start)  # T, N_t, segment table, tracker: as at the start
-            lp.flags[:, :nmax0].copy_(s0["st"].flags)  # the selection made before the stretch (held until a boundary)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            gl_.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            return e0.elapsed_time(e1) * 1e3 / n_tok
-        loop_run()
-        us = loop_run()
-        lp.check_status()
+            def loop_run():
+                lp.start_from(bpad, inp0.num_summaries, start)  # T, N_t, segment table, tracker: as at the start
+                lp.flags[:, :nmax0].copy_(s0["st"].flags)  # the selection before the stretch (held to a boundary)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                gl_.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                return e0.elapsed_time(e1) * 1e3 / n_tok
+            loop_run()
+            us = loop_run()
+            lp.check_status()
+            return lp, us
+        lp, us = loop_time()
         n_closed = int(lp.num_summaries[0]) - int(inp0.num_summaries[0])
+        del lp
+        _, us_sep = loop_time(chained=False, fused_a0=False)
         decode_loop = {"us_per_token": us, "tokens": n_tok, "selection_updates": sum(t == 200 for t in toks),
-                       "summaries_closed": n_closed, "launches_per_token": 5,
-                       "note": "append + segment tracking + fused select (a1 at summary closures, a2/a3 at "
-                       "sentence boundaries only) + a5; the 256 steps captured in one CUDA graph"}
+                       "summaries_closed": n_closed, "launches_per_token": 3,
+                       "separate_us_per_token": us_sep,
+                       "note": "zoomr_append_track (append + segment tracking, PDL behind the chained a5) + fused "
+                       "select (a1 at summary closures, a2/a3 at sentence boundaries only) + chained a5; the "
+                       "256 steps captured in one CUDA graph.  separate_us_per_token: append + advance, track, select, "
+                       "plain a5 as 5 plain launches (the round-1 loop)"}
     # the paper's comparison policies on the same kernels (NEXT-3), informational:
     # StreamingLLM at ZoomR's budget (mean |I_f|), SumR (all summaries kept): a4 + a5 per step;
     # H2O at the same budget: eviction by cumulative attention + a5 with logits + accumulation

@@ -360,6 +360,19 @@ int zoomr_tier_gather_slice(const zoomr_geom *geom, int32_t batch, const zoomr_k
                             int32_t layer_count, void *slice_k, void *slice_v, int32_t slice_page_size,
                             int32_t slice_pages_per_seq, int32_t *dev_status, void *stream);
 
+/* zoomr_append_kv + zoomr_track_segments in ONE launch (ABI 9): the token's
+ * rows at position T = seq_len[b], then seq_len[b] = T + 1, then the tracking of
+ * position T -- the same results as the two calls.  Right behind the library's
+ * chained a5 it is launched with PDL and overlaps that a5's end (a5 has read
+ * seq_len in its prologue and reads no row at position T); it completes only
+ * after that a5, so the next launch (the selection, which rewrites I_f) does not
+ * overlap the a5.  Arguments as the two calls. */
+int zoomr_append_track(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
+                       const void *v_new, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
+                       const int32_t *boundary_ids, int32_t n_boundary, int32_t *seq_len, int32_t *bounds,
+                       int32_t *num_summaries, int32_t max_summaries, int32_t *state, int32_t *close_items,
+                       uint8_t *update, int32_t *dev_status, void *stream);
+
 /* ---- Token-sharded split-K across GPUs (H_kv < #GPUs) --------
  *
  * The KV cache of a sequence is spread over R ranks by token (owner[b][t] = the

@@ -167,22 +167,27 @@ class ZoomrStep:
 class DecodeLoop(ZoomrStep):
     """Algorithm 1's whole decode step on the device:
 
-        a0 append k_t, v_t        zoomr_append_kv          (T += 1)
-        segment tracking          zoomr_track_segments     (delimiters -> segment table,
-                                                            closed summary -> a1 item,
-                                                            boundary token -> update flag)
+        a0 append k_t, v_t        zoomr_append_track       (T += 1; one launch with
+        segment tracking                                    the tracking: delimiters ->
+                                                            segment table, closed summary
+                                                            -> a1 item, boundary token ->
+                                                            update flag)
         a1..a4                    zoomr_select_fused       (a2/a3 only where update[b])
-        a5                        zoomr_sparse_decode_attn (early rows)
+        a5                        zoomr_sparse_decode_attn (early rows; chained: its end
+                                                            overlaps the next a0)
 
     No host decision in between, so a step is one CUDA-graph replay.  The
     segment table, N_t and T live on the device (`bounds`, `num_summaries`,
-    `seq_len`), initialised from the prompt by `start()`."""
+    `seq_len`), initialised from the prompt by `start()`.  fused_a0=False issues
+    zoomr_append_kv + zoomr_track_segments instead (same results)."""
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int,
                  params: StepParams, begin_id: int, end_id: int, boundary_ids, device="cuda",
-                 debug_outputs: bool = False, early_known: bool = True):
+                 debug_outputs: bool = False, early_known: bool = True, chained: bool = True,
+                 fused_a0: bool = True):
         super().__init__(shape, batch, max_summaries, index_capacity, params, device, debug_outputs,
-                         early_known=early_known)
+                         early_known=early_known, chained=chained)
+        self.fused_a0 = fused_a0
         dev = torch.device(device)
         self.begin_id, self.end_id = int(begin_id), int(end_id)
         self.boundary_ids = torch.as_tensor(list(boundary_ids), dtype=torch.int32, device=dev)
@@ -218,12 +223,17 @@ class DecodeLoop(ZoomrStep):
         """Enqueue one step; k_new/v_new bf16 [B][L][H_kv][d], q bf16 [B][L][H_q][d], token_ids int32 [B]."""
         k_pool, v_pool, page_table = kv
         p = self.params
-        Z.append_kv(self.shape, k_pool, v_pool, page_table, k_new, v_new, self.seq_len, self.status)
-        Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
-                         self.num_summaries, self.track_state, self.close_items, self.update, self.status)
+        if self.fused_a0:
+            Z.append_track(self.shape, k_pool, v_pool, page_table, k_new, v_new, token_ids, self.begin_id,
+                           self.end_id, self.boundary_ids, self.seq_len, self.bounds, self.num_summaries,
+                           self.track_state, self.close_items, self.update, self.status)
+        else:
+            Z.append_kv(self.shape, k_pool, v_pool, page_table, k_new, v_new, self.seq_len, self.status)
+            Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
+                             self.num_summaries, self.track_state, self.close_items, self.update, self.status)
         Z.select_fused(self.shape, q, k_pool, v_pool, page_table, self.bounds, self.num_summaries, self.seq_len,
                        self.close_items, self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags, self.index,
                        self.count, self.sel_workspace, partial=self.partial, agreeability=self.agreeability,
                        alpha_out=self.alpha, topk_out=self.topk, dev_status=self.status, update=self.update)
-        self.attend(q, kv, self.seq_len)
+        self.attend(q, kv, self.seq_len, chained=self.chained)
         return self.out

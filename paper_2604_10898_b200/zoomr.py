@@ -27,8 +27,8 @@ EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_
            "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
            "zoomr_write_newest_kv", "zoomr_sparse_decode_attn_chained", "zoomr_select_fused_chained",
-           "zoomr_select_front", "zoomr_select_tail", "zoomr_tier_gather_slice", "zoomr_status_str",
-           "zoomr_abi_version")
+           "zoomr_select_front", "zoomr_select_tail", "zoomr_tier_gather_slice", "zoomr_append_track",
+           "zoomr_status_str", "zoomr_abi_version")
 
 
 class ZoomrError(RuntimeError):
@@ -87,6 +87,9 @@ def lib():
         L.zoomr_append_kv.restype = C.c_int
         L.zoomr_track_segments.argtypes = [i32, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp]
         L.zoomr_track_segments.restype = C.c_int
+        L.zoomr_append_track.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp,
+                                         vp]
+        L.zoomr_append_track.restype = C.c_int
         L.zoomr_shard_index.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp]
         L.zoomr_shard_index.restype = C.c_int
         L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, i32, i32,
@@ -486,6 +489,21 @@ def write_newest_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_
     _check("zoomr_write_newest_kv", rc)
 
 
+def append_track(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, token_ids, begin_id, end_id, boundary_ids,
+                 seq_len, bounds, num_summaries, state, close_items, update, dev_status=None, stream=None):
+    """zoomr_append_track: append_kv + track_segments in one launch (PDL behind a chained a5)."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    nb = 0 if boundary_ids is None else boundary_ids.numel()
+    rc = lib().zoomr_append_track(
+        C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"), _ptr(v_new, torch.bfloat16, "v_new"),
+        _ptr(token_ids, torch.int32, "token_ids"), int(begin_id), int(end_id),
+        _ptr(boundary_ids, torch.int32, "boundary_ids") if nb else None, nb, _ptr(seq_len, torch.int32, "seq_len"),
+        _ptr(bounds, torch.int32, "bounds"), _ptr(num_summaries, torch.int32, "num_summaries"), bounds.shape[1],
+        _ptr(state, torch.int32, "state"), _ptr(close_items, torch.int32, "close_items"),
+        _ptr(update, torch.uint8, "update"), _ptr(dev_status, torch.int32, "dev_status"), _stream(stream))
+    _check("zoomr_append_track", rc)
+
+
 def track_segments(token_ids, begin_id, end_id, boundary_ids, seq_len, bounds, num_summaries, state,
                    close_items, update, dev_status=None, stream=None):
     """zoomr_track_segments: summary delimiters / semantic boundaries of the token just appended."""
@@ -505,7 +523,7 @@ _STAGES = {
     "sparse_decode_attn": "a5", "select_fused": "a1-a4", "select_front": "a1-a2", "select_tail": "a3-a4", "append_kv": "a0", "track_segments": "a0",
     "shard_index": "a4-shard", "sparse_decode_attn_lse": "a5-lse", "merge_attn": "a5-merge",
     "sparse_decode_attn_logits": "a5-logits", "h2o_accumulate": "h2o", "h2o_select": "h2o",
-    "tier_fetch": "tier", "write_newest_kv": "a0-tier", "tier_gather_slice": "tier-slice",
+    "tier_fetch": "tier", "write_newest_kv": "a0-tier", "append_track": "a0", "tier_gather_slice": "tier-slice",
 }
 
 

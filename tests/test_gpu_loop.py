@@ -51,8 +51,11 @@ def bits(t):
     return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("graph", [False, True])
-def test_decode_loop_matches_oracle_loop(graph):
+@pytest.mark.parametrize("graph,chained,fused_a0", [(False, True, True), (True, True, True), (True, False, False),
+                                                    (False, False, True)])
+def test_decode_loop_matches_oracle_loop(graph, chained, fused_a0):
+    """chained + fused_a0 (the default): zoomr_append_track launched with PDL behind the
+    chained a5 of the previous step; otherwise plain launches / separate append + track."""
     from paper_2604_10898_b200 import zoomr as Z
     from paper_2604_10898_b200.step import DecodeLoop, StepParams
     B, L, Hq, Hkv, d, P = 2, 2, 8, 2, 64, 16
@@ -76,7 +79,8 @@ def test_decode_loop_matches_oracle_loop(graph):
             v_pool[:, pg, :, sl] = prompt_v[b, t]
     kv = (k_pool.cuda(), v_pool.cuda(), page_table.cuda())
     shape = Z.Shape(L, Hq, Hkv, d, P)
-    loop = DecodeLoop(shape, B, MS, T_max, StepParams(top_k, c, sink, window), BEGIN, END, BOUNDARY)
+    loop = DecodeLoop(shape, B, MS, T_max, StepParams(top_k, c, sink, window), BEGIN, END, BOUNDARY,
+                      chained=chained, fused_a0=fused_a0)
     loop.start(n_p)
     refs = [OracleLoop(L, Hq, Hkv, d, top_k, c, sink, window, BEGIN, END, BOUNDARY,
                        list(bits(prompt_k[b])), list(bits(prompt_v[b]))) for b in range(B)]
@@ -121,3 +125,50 @@ def test_decode_loop_matches_oracle_loop(graph):
                 assert np.array_equal(loop.partial[b, 0, :n].cpu().numpy(), r["votes"]), (t, b)
     assert n_updates >= 10
     assert min(int(x) for x in loop.num_summaries.cpu()) >= 4
+
+
+def test_chained_loop_graph_equals_plain_loop():
+    """Many decode steps back to back in ONE graph (append_track of step t+1 overlapping the
+    end of step t's chained a5): every output of every step bit-identical to the plain
+    5-launch loop, and the final segment table / T equal."""
+    from paper_2604_10898_b200 import zoomr as Z
+    from paper_2604_10898_b200.step import DecodeLoop, StepParams
+    B, L, Hq, Hkv, d, P = 3, 2, 8, 2, 128, 32
+    n_p, steps, MS = 300, 96, 16
+    T_max = n_p + steps
+    gen = torch.Generator(device="cpu").manual_seed(9)
+    pages = (T_max + P - 1) // P
+    k_pool = torch.randn(L, B * pages, Hkv, P, d, generator=gen).bfloat16().cuda()
+    v_pool = torch.randn(L, B * pages, Hkv, P, d, generator=gen).bfloat16().cuda()
+    page_table = torch.randperm(B * pages, generator=gen).int().view(B, pages).cuda()
+    streams = [token_stream(np.random.default_rng(20 + b), steps) for b in range(B)]
+    toks = torch.tensor([[streams[b][t] for b in range(B)] for t in range(steps)], dtype=torch.int32).cuda()
+    k_new = torch.randn(steps, B, L, Hkv, d, generator=gen).bfloat16().cuda()
+    v_new = torch.randn(steps, B, L, Hkv, d, generator=gen).bfloat16().cuda()
+    q = (0.25 * torch.randn(steps, B, L, Hq, d, generator=gen)).bfloat16().cuda()
+    shape = Z.Shape(L, Hq, Hkv, d, P)
+    res = []
+    for chained, fused_a0 in ((True, True), (False, False)):
+        kv = (k_pool.clone(), v_pool.clone(), page_table)
+        lp = DecodeLoop(shape, B, MS, T_max, StepParams(2, 2, 4, 64), BEGIN, END, BOUNDARY, chained=chained,
+                        fused_a0=fused_a0)
+        lp.start(n_p)
+        outs = torch.zeros(steps, *lp.out.shape, device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for t in range(steps):
+                lp.decode_step(kv, k_new[t], v_new[t], q[t], toks[t])
+                outs[t].copy_(lp.out)
+        lp.start(n_p)
+        g.replay()
+        torch.cuda.synchronize()
+        lp.check_status()
+        res.append(dict(outs=outs, seq_len=lp.seq_len.clone(), bounds=lp.bounds.clone(),
+                        num_summaries=lp.num_summaries.clone(), flags=lp.flags.clone(), k=kv[0], v=kv[1]))
+    a, b = res
+    assert int(a["num_summaries"].min()) >= 2
+    for k in ("seq_len", "bounds", "num_summaries", "flags", "k", "v"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["outs"], b["outs"])

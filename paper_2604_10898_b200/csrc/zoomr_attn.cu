@@ -437,6 +437,10 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
 
   if (producer) {
     // ================= producer: address pipeline + TMA / cp.async copies =====
+    TL(8);
+#ifdef ZOOMR_TL_RAMP
+    TLW_SET(gw, 4, clock64());
+#endif
     // A(k+4): I_f position   B(k+2): page-table entry   C(k): row copies.
     // Each dependent load is consumed two iterations after it is issued, so the
     // index -> page -> row chain never stalls the copy issue in steady state.
@@ -508,6 +512,12 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       }
       if (k >= ntiles) break;
       if (k + kAheadA < ntiles) stage_a(k + kAheadA, q4);
+      if (k == -kAheadA) {
+        TL(9);
+#ifdef ZOOMR_TL_RAMP
+        TLW_SET(gw, 5, clock64());
+#endif
+      }
       if (k + kAheadB >= kfill && k + kAheadB < ntiles) stage_b(q2);
       if (k < kfill) {
         q0 = q1;
@@ -557,15 +567,24 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       const bool lead32 = whole && cok && pos == 0;
       const bool lead16 = S::SWZ && !whole && cok && pos < n16 && (pos & 15) == 0;
       const bool lead8 = S::SWZ && !whole && cok && n8 && pos == n16;
-      const bool byhand = !cok || !S::SWZ || pos >= n16 + n8;
-      const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8);
+      // the last len % 8 rows of a run of >= 8: one more 8-row box ending at the run's
+      // end, overlapping the previous box (the overlapped rows are written twice with
+      // the same bytes); only runs shorter than 8 rows go through cp.async
+      const bool leadT = S::SWZ && !whole && cok && len >= 8 && (len & 7) && pos == len - 8;
+      const bool byhand = !cok || !S::SWZ || (len < 8 && pos >= n16 + n8);
+      const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8 || leadT);
       const uint32_t tx = (uint32_t)((__ballot_sync(0xffffffffu, lead32) ? 32 : 0) * S::RB * 2 +
                                      (__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);
       const int s = (int)(k % kStages);
       mbar_wait(&emptyp[s], (uint32_t)(((k / kStages) & 1) ^ 1), 6000000 + (int)k);
       const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
       const uint32_t stV = stK + S::TILE_BYTES;
-      if (k == 0) TL(7);
+      if (k == 0) {
+        TL(7);
+#ifdef ZOOMR_TL_RAMP
+        TLW_SET(gw, 3, clock64());
+#endif
+      }
       if (lane == 0) mbar_arrive_expect_tx(&fullp[s], tx);
       __syncwarp();
       // one issue block per box height: the tensor map (like the barrier and the
@@ -587,7 +606,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
           tma_load_2d(stV + off, &maps.v16, rg * S::BX, grow, &fullp[s]);
         }
       }
-      if (lead8) {
+      if (lead8 || leadT) {
 #pragma unroll
         for (int rg = 0; rg < S::NREG; ++rg) {
           const uint32_t off = (uint32_t)(rg * S::REG_BYTES + lane * S::RBR);
@@ -624,7 +643,7 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         TL(6);
         TLW_SET(gw, 6, TL_NOW());
       }
-#ifdef ZOOMR_TIMELINE
+#if defined(ZOOMR_TIMELINE) && !defined(ZOOMR_TL_RAMP)
       const unsigned tl_cp = __ballot_sync(0xffffffffu, byhand && cok);
       TLW_ADD(gw, 4, __popc(tl_cp));
       TLW_ADD(gw, 5, __popc(m16) + __popc(m8));
@@ -687,7 +706,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
   };
 
   auto flush = [&](int ph, int b, int seg, bool at_end) {
+#ifndef ZOOMR_TL_RAMP
     TLW_ADD(gw, 7, 1);
+#endif
     // At the warp's last flush: if every other part of the segment has already
     // arrived, this part is the last one -- merge right away, with this part
     // taken from shared memory, instead of publishing it, fencing and counting
@@ -954,7 +975,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       }
       if (lane == 0) *cnt = 0;  // leave the workspace zeroed for the next call
       TLW_ADD(gw, 2, 1);
+#ifndef ZOOMR_TL_RAMP
       TLW_ADD(gw, 3, TL_NOW() - tl_m0);
+#endif
     }
   };
 
@@ -1008,7 +1031,12 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     const int nvalid = min(kTile, cnt - tis * kTile);
     const int s = (int)(k % kStages);
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1), 5000000 + (int)k);
-    if (k == 0) TL(3);
+    if (k == 0) {
+      TL(3);
+#ifdef ZOOMR_TL_RAMP
+      TLW_SET(gw, 7, clock64());
+#endif
+    }
     if (k == nAk) TL(4);
     const uint32_t stK = ring + (uint32_t)(s * S::STAGE_BYTES);
     const uint32_t stV = stK + S::TILE_BYTES;

@@ -80,8 +80,8 @@ class HostTierStep(ZoomrStep):
 class TierDecodeLoop(HostTierStep):
     """Algorithm 1's whole decode step over the host tier, one CUDA-graph replay:
 
-        a0 append k_t, v_t        zoomr_append_kv into the HOST cache (write-through, T += 1)
-        segment tracking          zoomr_track_segments
+        a0 append k_t, v_t        zoomr_append_track: into the HOST cache (write-through,
+        + segment tracking        T += 1) and the tracking, one launch
         a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
                                   the host cache; a2/a3 only at semantic boundaries)
         newest rows -> hot pool   zoomr_write_newest_kv (resident after a warm step: the
@@ -135,12 +135,13 @@ class TierDecodeLoop(HostTierStep):
         previous step's fetch kept the next token's page resident, look-ahead)."""
         p, hs = self.params, self.host_shape
         early = self._warm
-        Z.append_kv(hs, self.host_k, self.host_v, self.page_table, k_new, v_new, self.seq_len, self.status)
+        # append into the host cache (write-through, T += 1) + segment tracking, one launch
+        Z.append_track(hs, self.host_k, self.host_v, self.page_table, k_new, v_new, token_ids, self.begin_id,
+                       self.end_id, self.boundary_ids, self.seq_len, self.bounds, self.num_summaries,
+                       self.track_state, self.close_items, self.update, self.status)
         # the newest rows into their hot page (resident after a warm step; else the fetch brings it)
         Z.write_newest_kv(self.shape, self.hot_k, self.hot_v, self.hot_page_table, k_new, v_new, self.seq_len,
                           self.status)
-        Z.track_segments(token_ids, self.begin_id, self.end_id, self.boundary_ids, self.seq_len, self.bounds,
-                         self.num_summaries, self.track_state, self.close_items, self.update, self.status)
         Z.select_fused(hs, q, self.host_k, self.host_v, self.page_table, self.bounds, self.num_summaries,
                        self.seq_len, self.close_items, self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags,
                        self.index, self.count, self.sel_workspace, partial=self.partial,

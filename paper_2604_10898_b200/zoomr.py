@@ -491,8 +491,9 @@ def write_newest_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_
 
 def append_track(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, token_ids, begin_id, end_id, boundary_ids,
                  seq_len, bounds, num_summaries, state, close_items, update, dev_status=None, stream=None):
-    """zoomr_append_track: append_kv + track_segments in one launch (PDL behind a chained a5)."""
-    g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
+    """zoomr_append_track: append_kv + track_segments in one launch (PDL behind a chained a5).
+    The pools may be pinned host tensors (the host tier)."""
+    g, kv = shape.c(), _kv(k_pool, v_pool, page_table, host_ok=True)
     nb = 0 if boundary_ids is None else boundary_ids.numel()
     rc = lib().zoomr_append_track(
         C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"), _ptr(v_new, torch.bfloat16, "v_new"),

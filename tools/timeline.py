@@ -32,7 +32,7 @@ def read(fn, reset):
 NAMES = {"select": ["start", "front_end", "tail_start", "collected", "topc_done", "end", "a1_done", "(unused)",
                     "score_topk_done"],
          "a5": ["start", "prologue", "B_known", "first_tile", "first_B_tile", "math_done", "prod_done",
-                "first_issue"]}
+                "first_issue", "prod_enter", "first_stage_a"]}
 for var in os.environ.get("VARS", "early,late").split(","):
     sets = []
     for r in range(4):
@@ -43,6 +43,12 @@ for var in os.environ.get("VARS", "early,late").split(","):
         st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))
         newest = torch.tensor([[0, int(inp.num_summaries[0]) - 1]], dtype=torch.int32, device="cuda")
         g = st.capture(inp.q, kv, seg, close_items=newest)
+        if os.environ.get("A5ONLY"):  # a graph of a5 alone (over the I_f the step above left)
+            st.run(inp.q, kv, seg, close_items=newest)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                st.attend(inp.q, kv, inp.seq_len if var == "early" else None)
         g.keep = (st, inp, newest)  # the graph uses their buffers
         sets.append(g)
     for i in range(12):
@@ -70,8 +76,9 @@ for var in os.environ.get("VARS", "early,late").split(","):
     print(f"== {var} ({cfg.name}), median over {len(samples)} steps, us after the first select CTA start")
     for who, idx in (("select", 0), ("a5", 1)):
         for m, name in enumerate(NAMES[who]):
-            lo = [s[idx][2 * m] - s[0][0] for s in samples if s[idx][2 * m] != 2**64 - 1]
-            hi = [s[idx][2 * m + 1] - s[0][0] for s in samples if s[idx][2 * m + 1]]
+            base = lambda s: s[0][0] if s[0][0] != 2**64 - 1 else s[1][0]  # A5ONLY: the first a5 CTA start
+            lo = [s[idx][2 * m] - base(s) for s in samples if s[idx][2 * m] != 2**64 - 1]
+            hi = [s[idx][2 * m + 1] - base(s) for s in samples if s[idx][2 * m + 1]]
             if lo:
                 print(f"  {who:6s} {m} {name:12s} {statistics.median(lo)/1e3:8.2f} .. {statistics.median(hi)/1e3:8.2f}")
 
@@ -140,3 +147,21 @@ if os.environ.get("WARPS"):
     X = np.c_[np.ones(len(M)), M[:, 4], M[:, 5], M[:, 3], M[:, 7]]
     coef, *_ = np.linalg.lstsq(X, M[:, 0], rcond=None)
     print("  fit end = %.2f + %.4f*cp_rows + %.4f*boxes + %.3f*merge_us + %.3f*flushes" % tuple(coef))
+
+# producer ramp in SM clocks (the ZOOMR_TL_RAMP build: fields 4 / 5 / 3 / 7 hold clock64 at
+# producer entry, after its first stage_a, at its first copy issue, and at its math warp's first tile)
+if os.environ.get("RAMP"):
+    import numpy as np
+    d1, d2, d3 = [], [], []
+    for i in range(int(os.environ.get("REPS", "8"))):
+        measured_step(i)
+        buf = (C.c_ulonglong * (4096 * 8))()
+        lib.zoomr_tl_warp_attn(buf)
+        for w in range(4096):
+            r = buf[8 * w: 8 * w + 8]
+            if r[4] and r[5] and r[3] and r[7]:
+                d1.append(r[5] - r[4]); d2.append(r[3] - r[5]); d3.append(r[7] - r[3])
+    for name, v in (("enter -> first stage_a", d1), ("first stage_a -> first issue", d2),
+                    ("first issue -> math warp's first tile", d3)):
+        v = np.array(v, dtype=np.float64)
+        print(f"  {name:40s} cycles p10 {np.percentile(v, 10):8.0f} p50 {np.median(v):8.0f} p90 {np.percentile(v, 90):8.0f}")

@@ -7,6 +7,9 @@
 
 namespace zoomr {
 
+#ifndef ZOOMR_SCORE_MARK
+#define ZOOMR_SCORE_MARK(i) do { } while (0)
+#endif
 constexpr int kHistBins = 2048;  // vote histogram bins of the top-c threshold search
 constexpr int kTopcRounds = 8;   // c <= this: the c largest votes by c block-max rounds, then the tie group
 constexpr int kTopcRoundsMinN = 192;  // ... when N_t is above this (below, direct ranking is cheaper:
@@ -130,8 +133,10 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
                                  float *__restrict__ alpha_out /* [G][ald_out] or null */, int64_t ald_out,
                                  int *sel_i /* smem [G][top_k] */, float *sel_a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int x = threadIdx.x; x < G * D; x += blockDim.x) qs[x] = __bfloat162float(qb[x]);
-  __syncthreads();
+  if (qb) {  // (null: the caller has staged qs already)
+    for (int x = threadIdx.x; x < G * D; x += blockDim.x) qs[x] = __bfloat162float(qb[x]);
+    __syncthreads();
+  }
   constexpr int FPL = D / 8;  // floats per octet lane
   constexpr int NV = FPL >= 4 ? FPL / 4 : 1;
   const int oct = lane >> 3, l8 = lane & 7;
@@ -154,6 +159,7 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
     }
   };
   const int step = nw * 8;
+  if (threadIdx.x == 0) ZOOMR_SCORE_MARK(10);
   if (warp * 8 < nt) load(warp * 8, kv, kv2);
   for (int base = warp * 8; base < nt; base += step) {
     if (base + step < nt) load(base + step, kn, kn2);
@@ -201,6 +207,7 @@ __device__ void block_score_topk(const __nv_bfloat16 *__restrict__ qb /* [G][D] 
       kv2[u] = kn2[u];
     }
   }
+  if (lane == 0) ZOOMR_SCORE_MARK(9);
   __syncthreads();
   const int kk = top_k < nt ? top_k : nt;
   for (int hh = warp; hh < G; hh += nw) {

@@ -24,9 +24,17 @@
 // Results are bit-identical to the standalone chain (same arithmetic, integer
 // aggregation).  Single-rank only: the KV-head-sharded mode needs the
 // all-reduce between a2 and a3 and uses the standalone entry points.
-#include "select_common.cuh"
+#include "common.cuh"
 
 ZOOMR_TL_STORAGE(fused)
+#ifdef ZOOMR_TIMELINE  // timeline builds: marks inside the scoring loop of the fused select
+#define ZOOMR_SCORE_MARK(i)                             \
+  do {                                                  \
+    const bool tl_on_ = *(volatile int *)&zoomr::g_tl_on; \
+    TL(i);                                              \
+  } while (0)
+#endif
+#include "select_common.cuh"
 
 namespace zoomr {
 
@@ -127,6 +135,18 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
     __syncthreads();
   }
 #endif
+  // the G queries of this (l, g): loaded now, so that the load overlaps a1's chain
+  // instead of adding a round trip between a1 and the scoring
+  constexpr int kQPT = (G * D + 255) / 256;  // per thread (256 threads)
+  float qreg[kQPT];
+  const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
+  if (!tail_only && !tail_cta) {
+#pragma unroll
+    for (int j = 0; j < kQPT; ++j) {
+      const int x = threadIdx.x + j * 256;
+      qreg[j] = x < G * D ? __bfloat162float(qb[x]) : 0.f;
+    }
+  }
   // ---- a1: mean keys of the summaries of b that closed this step -----------
   if (!tail_only && !tail_cta) {
     double *red = reinterpret_cast<double *>(smem_raw);  // [nwarps][D]
@@ -147,6 +167,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
                         l, g, s0, s1, red, mk + (int64_t)i * D, p.status);
     }
     __syncthreads();  // this CTA's own global writes are visible to it after the barrier
+    if (threadIdx.x == 0) TL(6);
   }
 
   // ---- a2: alpha + per-voter top-k (only at a selection update) ---------------------
@@ -156,9 +177,15 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
     float *al = qs + G * D;                                          // [G][MS]
     int *sel_i = reinterpret_cast<int *>(al + G * MS);               // [G][k]
     float *sel_a = reinterpret_cast<float *>(sel_i + G * p.top_k);   // [G][k]
-    const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
     float *ao = p.alpha_out ? p.alpha_out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * MS : nullptr;
-    block_score_topk<D, G>(qb, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
+#pragma unroll
+    for (int j = 0; j < kQPT; ++j) {
+      const int x = threadIdx.x + j * 256;
+      if (x < G * D) qs[x] = qreg[j];
+    }
+    __syncthreads();
+    block_score_topk<D, G>(nullptr, mk, nt, p.top_k, qs, al, MS, ao, MS, sel_i, sel_a);
+    if (threadIdx.x == 0) TL(8);
     const int kk = p.top_k < nt ? p.top_k : nt;
     for (int x = threadIdx.x; x < G * p.top_k; x += blockDim.x) {
       const int hh = x / p.top_k, r = x - hh * p.top_k;

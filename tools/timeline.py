@@ -30,7 +30,7 @@ def read(fn, reset):
 
 
 NAMES = {"select": ["start", "front_end", "tail_start", "collected", "topc_done", "end", "a1_done", "(unused)",
-                    "score_topk_done"],
+                    "score_topk_done", "score_loop_done(warp)", "score_loop_start"],
          "a5": ["start", "prologue", "B_known", "first_tile", "first_B_tile", "math_done", "prod_done",
                 "first_issue", "prod_enter", "first_stage_a"]}
 for var in os.environ.get("VARS", "early,late").split(","):

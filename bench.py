@@ -948,9 +948,9 @@ def run_ours(args):
         del lp
         _, us_sep = loop_time(chained=False, fused_a0=False)
         decode_loop = {"us_per_token": us, "tokens": n_tok, "selection_updates": sum(t == 200 for t in toks),
-                       "summaries_closed": n_closed, "launches_per_token": 3,
+                       "summaries_closed": n_closed, "launches_per_token": 4,
                        "separate_us_per_token": us_sep,
-                       "note": "zoomr_append_track (append + segment tracking, PDL behind the chained a5) + fused "
+                       "note": "zoomr_append_track (row copy + tracking kernel, PDL behind the chained a5) + fused "
                        "select (a1 at summary closures, a2/a3 at sentence boundaries only) + chained a5; the "
                        "256 steps captured in one CUDA graph.  separate_us_per_token: append + advance, track, select, "
                        "plain a5 as 5 plain launches (the round-1 loop)"}

@@ -360,13 +360,17 @@ int zoomr_tier_gather_slice(const zoomr_geom *geom, int32_t batch, const zoomr_k
                             int32_t layer_count, void *slice_k, void *slice_v, int32_t slice_page_size,
                             int32_t slice_pages_per_seq, int32_t *dev_status, void *stream);
 
-/* zoomr_append_kv + zoomr_track_segments in ONE launch (ABI 9): the token's
- * rows at position T = seq_len[b], then seq_len[b] = T + 1, then the tracking of
- * position T -- the same results as the two calls.  Right behind the library's
- * chained a5 it is launched with PDL and overlaps that a5's end (a5 has read
- * seq_len in its prologue and reads no row at position T); it completes only
- * after that a5, so the next launch (the selection, which rewrites I_f) does not
- * overlap the a5.  Arguments as the two calls. */
+/* zoomr_append_kv + zoomr_track_segments without a host round trip (ABI 9): the
+ * token's rows at position T = seq_len[b] (one CTA per (layer, sequence)), then a
+ * tracking kernel launched with PDL behind the row copy -- it starts once every
+ * row CTA has used T -- that tracks position T and sets seq_len[b] = T + 1.  The
+ * same results as the two calls.  Right behind the library's chained a5 the row
+ * copy is itself launched with PDL and overlaps that a5's end (a5 has read
+ * seq_len in its prologue and reads no row at position T); both kernels end with
+ * griddepcontrol.wait, so the call completes only after that a5 and the next
+ * launch (the selection, which rewrites I_f) does not overlap it.  The pools may
+ * be pinned host memory (the host tier's write-through).  Arguments as the two
+ * calls. */
 int zoomr_append_track(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
                        const void *v_new, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
                        const int32_t *boundary_ids, int32_t n_boundary, int32_t *seq_len, int32_t *bounds,

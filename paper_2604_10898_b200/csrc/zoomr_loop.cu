@@ -95,44 +95,57 @@ __global__ void track_kernel(int32_t batch, const int32_t *__restrict__ token_id
             n_boundary, bounds, num_summaries, max_summaries, state, close_items, update, status);
 }
 
-// a0 + segment tracking in one launch, one CTA per sequence: the token's rows at
-// position T = seq_len[b] (every layer and KV head), then T += 1 and the tracking
-// of position T.  Launched with PDL right behind a chained a5 it runs while that
-// a5 finishes: a5 read seq_len in its prologue (before its trigger) and reads no
-// row at position T; the final griddepcontrol.wait makes this launch complete
-// only after that a5, so the next kernel on the stream (the selection, which
-// rewrites I_f) never overlaps it.
-__global__ void append_track_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
-                                    __nv_bfloat16 *kpool, __nv_bfloat16 *vpool, int64_t num_pages,
-                                    const int32_t *__restrict__ page_table, int32_t max_pages, int32_t L,
-                                    int32_t Hkv, int32_t P, int32_t d, const int32_t *__restrict__ token_ids,
-                                    int32_t begin_id, int32_t end_id, const int32_t *__restrict__ boundary_ids,
-                                    int32_t n_boundary, int32_t *seq_len, int32_t *bounds, int32_t *num_summaries,
-                                    int32_t max_summaries, int4 *state, int32_t *close_items, uint8_t *update,
-                                    int32_t *status) {
-  const int b = blockIdx.x;
+// a0 + segment tracking as two launches that chain without a host round trip:
+//  * append_rows_kernel, one CTA per (layer, b) as append_kv: the token's rows at
+//    position T = seq_len[b]; each CTA triggers its dependents once it has used T;
+//  * track_advance_kernel (PDL behind it), one thread per sequence: the tracking of
+//    position T, then seq_len[b] = T + 1 -- launched only when every row CTA has
+//    read T, so no CTA can see the advanced T.
+// Right behind a chained a5 the row copy is launched with PDL and runs while that
+// a5 finishes (a5 read seq_len in its prologue, before its trigger, and reads no
+// row at position T).  Both kernels end with griddepcontrol.wait, so each
+// completes only after its predecessor: the next launch on the stream (the
+// selection, which rewrites I_f) is ordered after the a5 as well.
+__global__ void append_rows_kernel(const uint4 *__restrict__ k_new, const uint4 *__restrict__ v_new,
+                                   __nv_bfloat16 *kpool, __nv_bfloat16 *vpool, int64_t num_pages,
+                                   const int32_t *__restrict__ page_table, int32_t max_pages, int32_t L, int32_t Hkv,
+                                   int32_t P, int32_t d, const int32_t *__restrict__ seq_len, int32_t *status) {
+  const int b = blockIdx.y, l = blockIdx.x;
   const int T = seq_len[b];
   const int lp = T / P;
   const int page = (T >= 0 && lp < max_pages) ? page_table[(int64_t)b * max_pages + lp] : -1;
-  if (page < 0 || page >= num_pages) {
+  const bool ok = page >= 0 && page < num_pages;
+  const int64_t row = ok ? (((int64_t)l * num_pages + page) * Hkv * P + (T - lp * P)) : 0;
+  __syncthreads();            // every thread of the CTA has used T
+  allow_dependents();         // (the tracking may now advance seq_len)
+  if (!ok) {
     if (threadIdx.x == 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
   } else {
     const int cpr = d / 8;  // 16-byte chunks per row
-    for (int x = threadIdx.x; x < L * Hkv * cpr; x += blockDim.x) {
-      const int c = x % cpr, lg = x / cpr, g = lg % Hkv, l = lg / Hkv;
+    for (int x = threadIdx.x; x < Hkv * cpr; x += blockDim.x) {
+      const int g = x / cpr, c = x - g * cpr;
       const int64_t src = (((int64_t)b * L + l) * Hkv + g) * cpr + c;
-      const int64_t dst = (((((int64_t)l * num_pages + page) * Hkv + g) * P + (T - lp * P)) * d) / 8 + c;
+      const int64_t dst = ((row + (int64_t)g * P) * d) / 8 + c;
       reinterpret_cast<uint4 *>(kpool)[dst] = k_new[src];
       reinterpret_cast<uint4 *>(vpool)[dst] = v_new[src];
     }
   }
-  __syncthreads();  // every thread has read seq_len[b]
-  if (threadIdx.x == 0) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the preceding kernel
+}
+
+__global__ void track_advance_kernel(int32_t batch, const int32_t *__restrict__ token_ids, int32_t begin_id,
+                                     int32_t end_id, const int32_t *__restrict__ boundary_ids, int32_t n_boundary,
+                                     int32_t *seq_len, int32_t *bounds, int32_t *num_summaries,
+                                     int32_t max_summaries, int4 *state, int32_t *close_items, uint8_t *update,
+                                     int32_t *status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch) {
+    const int T = seq_len[b];
     seq_len[b] = T + 1;
     track_one(b, token_ids[b], T, begin_id, end_id, boundary_ids, n_boundary, bounds, num_summaries, max_summaries,
               state, close_items, update, status);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the preceding kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the row copy
 }
 
 }  // namespace zoomr
@@ -194,19 +207,20 @@ extern "C" int zoomr_append_track(const zoomr_geom *geom, int32_t batch, const z
       !bounds || !num_summaries || max_summaries < 1 || !state || !close_items || !update)
     return ZOOMR_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  auto kfn = append_track_kernel;
-  // with PDL only right behind the library's chained a5 (see the kernel's comment)
+  const dim3 grid(geom->num_layers, batch);
+  // the row copy with PDL only right behind the library's chained a5 (see the kernels' comment)
   if (prev_launch_is(s, kLaunchA5Chained, nullptr))
-    launch_pdl(kfn, dim3(batch), 256, 0, s, (const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k,
-               (__nv_bfloat16 *)kv->v, kv->num_pages, kv->page_table, kv->max_pages, geom->num_layers,
-               geom->num_kv_heads, geom->page_size, geom->head_dim, token_ids, begin_id, end_id, boundary_ids,
-               n_boundary, seq_len, bounds, num_summaries, max_summaries, reinterpret_cast<int4 *>(state),
-               close_items, update, dev_status);
+    launch_pdl(append_rows_kernel, grid, 128, 0, s, (const uint4 *)k_new, (const uint4 *)v_new,
+               (__nv_bfloat16 *)kv->k, (__nv_bfloat16 *)kv->v, kv->num_pages, kv->page_table, kv->max_pages,
+               geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim, (const int32_t *)seq_len,
+               dev_status);
   else
-    kfn<<<batch, 256, 0, s>>>((const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k,
-                              (__nv_bfloat16 *)kv->v, kv->num_pages, kv->page_table, kv->max_pages, geom->num_layers,
-                              geom->num_kv_heads, geom->page_size, geom->head_dim, token_ids, begin_id, end_id,
-                              boundary_ids, n_boundary, seq_len, bounds, num_summaries, max_summaries,
-                              reinterpret_cast<int4 *>(state), close_items, update, dev_status);
+    append_rows_kernel<<<grid, 128, 0, s>>>((const uint4 *)k_new, (const uint4 *)v_new, (__nv_bfloat16 *)kv->k,
+                                            (__nv_bfloat16 *)kv->v, kv->num_pages, kv->page_table, kv->max_pages,
+                                            geom->num_layers, geom->num_kv_heads, geom->page_size, geom->head_dim,
+                                            (const int32_t *)seq_len, dev_status);
+  launch_pdl(track_advance_kernel, dim3((batch + 127) / 128), 128, 0, s, batch, token_ids, begin_id, end_id,
+             boundary_ids, n_boundary, seq_len, bounds, num_summaries, max_summaries, reinterpret_cast<int4 *>(state),
+             close_items, update, dev_status);
   return launch_status(s);
 }

@@ -167,11 +167,11 @@ class ZoomrStep:
 class DecodeLoop(ZoomrStep):
     """Algorithm 1's whole decode step on the device:
 
-        a0 append k_t, v_t        zoomr_append_track       (T += 1; one launch with
-        segment tracking                                    the tracking: delimiters ->
-                                                            segment table, closed summary
-                                                            -> a1 item, boundary token ->
-                                                            update flag)
+        a0 append k_t, v_t        zoomr_append_track       (row copy + tracking kernel
+        segment tracking                                    chained by PDL, T += 1:
+                                                            delimiters -> segment table,
+                                                            closed summary -> a1 item,
+                                                            boundary token -> update flag)
         a1..a4                    zoomr_select_fused       (a2/a3 only where update[b])
         a5                        zoomr_sparse_decode_attn (early rows; chained: its end
                                                             overlaps the next a0)

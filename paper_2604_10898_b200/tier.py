@@ -81,7 +81,7 @@ class TierDecodeLoop(HostTierStep):
     """Algorithm 1's whole decode step over the host tier, one CUDA-graph replay:
 
         a0 append k_t, v_t        zoomr_append_track: into the HOST cache (write-through,
-        + segment tracking        T += 1) and the tracking, one launch
+        + segment tracking        T += 1) and the tracking, chained by PDL
         a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
                                   the host cache; a2/a3 only at semantic boundaries)
         newest rows -> hot pool   zoomr_write_newest_kv (resident after a warm step: the

@@ -420,6 +420,17 @@ int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batch, const vo
                                  int32_t layer_begin, int32_t layer_count, float *out, float *lse,
                                  void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
 
+/* zoomr_sparse_decode_attn_lse with the chained trigger of
+ * zoomr_sparse_decode_attn_chained (ABI 9): a PDL-launched successor -- the host
+ * tier's next zoomr_append_track -- may start once every CTA has passed its
+ * wait.  Same arguments and results. */
+int zoomr_sparse_decode_attn_lse_chained(const zoomr_geom *geom, int32_t batch, const void *q,
+                                         const zoomr_kv *kv, const int32_t *index, const int32_t *index_phys,
+                                         const int32_t *index_count, int32_t index_capacity,
+                                         const int32_t *seq_len, int32_t sink, int32_t window, float softmax_scale,
+                                         int32_t layer_begin, int32_t layer_count, float *out, float *lse,
+                                         void *workspace, size_t workspace_bytes, int32_t *dev_status, void *stream);
+
 /* Combine n_parts partial attention results (normally the all-gathered outputs
  * of zoomr_sparse_decode_attn_lse on each rank, over disjoint index sets):
  *   part_out fp32 [n_parts][B][L][H_q][d], part_lse fp32 [n_parts][B][L][H_q],

@@ -1352,6 +1352,19 @@ extern "C" int zoomr_sparse_decode_attn_lse(const zoomr_geom *geom, int32_t batc
                             stream);
 }
 
+extern "C" int zoomr_sparse_decode_attn_lse_chained(const zoomr_geom *geom, int32_t batch, const void *q,
+                                                    const zoomr_kv *kv, const int32_t *index,
+                                                    const int32_t *index_phys, const int32_t *index_count,
+                                                    int32_t index_capacity, const int32_t *seq_len, int32_t sink,
+                                                    int32_t window, float softmax_scale, int32_t layer_begin,
+                                                    int32_t layer_count, float *out, float *lse, void *workspace,
+                                                    size_t workspace_bytes, int32_t *dev_status, void *stream) {
+  if (!lse) return ZOOMR_ERR_INVALID_ARG;
+  return sparse_decode_attn(geom, batch, q, kv, index, index_phys, index_count, index_capacity, seq_len, sink, window,
+                            softmax_scale, layer_begin, layer_count, out, lse, workspace, workspace_bytes, dev_status,
+                            stream, nullptr, true);
+}
+
 extern "C" int zoomr_sparse_decode_attn_logits(const zoomr_geom *geom, int32_t batch, const void *q,
                                                const zoomr_kv *kv, const int32_t *index, const int32_t *index_count,
                                                int32_t index_capacity, float softmax_scale, float *out, float *lse,

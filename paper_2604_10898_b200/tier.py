@@ -93,9 +93,10 @@ class TierDecodeLoop(HostTierStep):
 
     def __init__(self, shape: Z.Shape, batch: int, max_summaries: int, index_capacity: int, params: StepParams,
                  host_k, host_v, page_table, hot_pages: int, begin_id: int, end_id: int, boundary_ids,
-                 device="cuda", hot_page_size: int = 0):
+                 device="cuda", hot_page_size: int = 0, chained: bool = True):
         super().__init__(shape, batch, max_summaries, index_capacity, params, host_k, host_v, page_table, hot_pages,
                          device, hot_page_size)
+        self.chained = chained
         dev = self.out.device
         self.begin_id, self.end_id = int(begin_id), int(end_id)
         self.boundary_ids = torch.as_tensor(list(boundary_ids), dtype=torch.int32, device=dev)
@@ -152,7 +153,8 @@ class TierDecodeLoop(HostTierStep):
                      seq_len=self.seq_len)  # (look-ahead: the next token's page)
         Z.sparse_decode_attn_lse(self.shape, q, self.hot_k, self.hot_v, self.hot_page_table, self.index, self.count,
                                  self.out, self.lse, self.workspace, dev_status=self.status,
-                                 seq_len=self.seq_len if early else None, sink=p.sink, window=p.window)
+                                 seq_len=self.seq_len if early else None, sink=p.sink, window=p.window,
+                                 chained=self.chained)  # (the next token's row copy may overlap its end)
         self._warm = True
         return self.out
 

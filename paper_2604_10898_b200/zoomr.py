@@ -24,7 +24,7 @@ A_FRAC_BITS = 32  # ZOOMR_A_FRAC_BITS
 EXPORTS = ("zoomr_update_mean_keys", "zoomr_score", "zoomr_select_topc", "zoomr_build_index",
            "zoomr_attn_workspace_bytes", "zoomr_sparse_decode_attn", "zoomr_select_workspace_bytes",
            "zoomr_select_fused", "zoomr_append_kv", "zoomr_track_segments", "zoomr_shard_index",
-           "zoomr_sparse_decode_attn_lse", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
+           "zoomr_sparse_decode_attn_lse", "zoomr_sparse_decode_attn_lse_chained", "zoomr_merge_attn", "zoomr_sparse_decode_attn_logits",
            "zoomr_h2o_accumulate", "zoomr_h2o_select", "zoomr_tier_workspace_bytes", "zoomr_tier_fetch",
            "zoomr_write_newest_kv", "zoomr_sparse_decode_attn_chained", "zoomr_select_fused_chained",
            "zoomr_select_front", "zoomr_select_tail", "zoomr_tier_gather_slice", "zoomr_append_track",
@@ -95,6 +95,9 @@ def lib():
         L.zoomr_sparse_decode_attn_lse.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, i32, i32,
                                                    vp, vp, vp, sz, vp, vp]
         L.zoomr_sparse_decode_attn_lse.restype = C.c_int
+        L.zoomr_sparse_decode_attn_lse_chained.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, i32, C.c_float, i32, i32,
+                                                   vp, vp, vp, sz, vp, vp]
+        L.zoomr_sparse_decode_attn_lse_chained.restype = C.c_int
         L.zoomr_merge_attn.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.zoomr_merge_attn.restype = C.c_int
         L.zoomr_sparse_decode_attn_logits.argtypes = [vp, i32, vp, vp, vp, vp, i32, C.c_float, vp, vp, vp, vp, sz,
@@ -267,11 +270,13 @@ def sparse_decode_attn(shape: Shape, q, k_pool, v_pool, page_table, index, index
 
 def sparse_decode_attn_lse(shape: Shape, q, k_pool, v_pool, page_table, index, index_count, out, lse,
                            workspace, softmax_scale=None, dev_status=None, stream=None, index_phys=None,
-                           layer_begin=0, layer_count=0, seq_len=None, sink=0, window=0):
-    """a5 over any index list, also writing lse fp32 [B][L][H_q] (zoomr_sparse_decode_attn_lse)."""
+                           layer_begin=0, layer_count=0, seq_len=None, sink=0, window=0, chained=False):
+    """a5 over any index list, also writing lse fp32 [B][L][H_q] (zoomr_sparse_decode_attn_lse;
+    chained: zoomr_sparse_decode_attn_lse_chained)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table)
     sc = shape.head_dim ** -0.5 if softmax_scale is None else float(softmax_scale)
-    rc = lib().zoomr_sparse_decode_attn_lse(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
+    fn = lib().zoomr_sparse_decode_attn_lse_chained if chained else lib().zoomr_sparse_decode_attn_lse
+    rc = fn(C.byref(g), q.shape[0], _ptr(q, torch.bfloat16, "q"),
                                             C.byref(kv), _ptr(index, torch.int32, "index"),
                                             _ptr(index_phys, torch.int32, "index_phys"),
                                             _ptr(index_count, torch.int32, "index_count"), index.shape[1],

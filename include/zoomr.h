@@ -369,10 +369,14 @@ int zoomr_tier_gather_slice(const zoomr_geom *geom, int32_t batch, const zoomr_k
  * seq_len in its prologue and reads no row at position T); both kernels end with
  * griddepcontrol.wait, so the call completes only after that a5 and the next
  * launch (the selection, which rewrites I_f) does not overlap it.  The pools may
- * be pinned host memory (the host tier's write-through).  Arguments as the two
- * calls. */
-int zoomr_append_track(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const void *k_new,
-                       const void *v_new, const int32_t *token_ids, int32_t begin_id, int32_t end_id,
+ * be pinned host memory (the host tier's write-through).  mirror (nullable,
+ * page size mirror_page_size, its own page table): a second pool that also gets
+ * the rows where their page is resident (entry -1: skipped, as
+ * zoomr_write_newest_kv) -- the host tier's HBM hot pool, in the same launch.
+ * Other arguments as the two calls. */
+int zoomr_append_track(const zoomr_geom *geom, int32_t batch, const zoomr_kv *kv, const zoomr_kv *mirror,
+                       int32_t mirror_page_size, const void *k_new, const void *v_new, const int32_t *token_ids,
+                       int32_t begin_id, int32_t end_id,
                        const int32_t *boundary_ids, int32_t n_boundary, int32_t *seq_len, int32_t *bounds,
                        int32_t *num_summaries, int32_t max_summaries, int32_t *state, int32_t *close_items,
                        uint8_t *update, int32_t *dev_status, void *stream);

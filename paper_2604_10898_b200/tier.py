@@ -81,11 +81,12 @@ class TierDecodeLoop(HostTierStep):
     """Algorithm 1's whole decode step over the host tier, one CUDA-graph replay:
 
         a0 append k_t, v_t        zoomr_append_track: into the HOST cache (write-through,
-        + segment tracking        T += 1) and the tracking, chained by PDL
+        + segment tracking        T += 1) and, mirrored, into the token's hot page when it
+                                  is resident (after a warm step it is: the previous fetch
+                                  made the page of T resident, look-ahead); the tracking
+                                  kernel chained by PDL
         a1..a4                    zoomr_select_fused (a1 reads the closing summary's rows from
                                   the host cache; a2/a3 only at semantic boundaries)
-        newest rows -> hot pool   zoomr_write_newest_kv (resident after a warm step: the
-                                  previous fetch made the page of T resident, look-ahead)
         tier fetch                zoomr_tier_fetch (pages that entered I_f + the look-ahead page)
         a5                        zoomr_sparse_decode_attn_lse on the hot pool, with the
                                   early rows (sink / window before the wait) once warm
@@ -136,13 +137,14 @@ class TierDecodeLoop(HostTierStep):
         previous step's fetch kept the next token's page resident, look-ahead)."""
         p, hs = self.params, self.host_shape
         early = self._warm
-        # append into the host cache (write-through, T += 1) + segment tracking, one launch
+        # append into the host cache (write-through, T += 1) and into the token's hot page
+        # when it is resident (after a warm step it is; else the fetch brings it), then
+        # the segment tracking -- one call
+        # (a separate zoomr_write_newest_kv after the tracking: +2.1 us per token, same-box A/B)
         Z.append_track(hs, self.host_k, self.host_v, self.page_table, k_new, v_new, token_ids, self.begin_id,
                        self.end_id, self.boundary_ids, self.seq_len, self.bounds, self.num_summaries,
-                       self.track_state, self.close_items, self.update, self.status)
-        # the newest rows into their hot page (resident after a warm step; else the fetch brings it)
-        Z.write_newest_kv(self.shape, self.hot_k, self.hot_v, self.hot_page_table, k_new, v_new, self.seq_len,
-                          self.status)
+                       self.track_state, self.close_items, self.update, self.status,
+                       mirror=(self.hot_k, self.hot_v, self.hot_page_table), mirror_page_size=self.shape.page_size)
         Z.select_fused(hs, q, self.host_k, self.host_v, self.page_table, self.bounds, self.num_summaries,
                        self.seq_len, self.close_items, self.mean_keys, p.top_k, p.c, p.sink, p.window, self.flags,
                        self.index, self.count, self.sel_workspace, partial=self.partial,

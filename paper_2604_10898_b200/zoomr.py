@@ -87,8 +87,8 @@ def lib():
         L.zoomr_append_kv.restype = C.c_int
         L.zoomr_track_segments.argtypes = [i32, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp]
         L.zoomr_track_segments.restype = C.c_int
-        L.zoomr_append_track.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp, vp, vp,
-                                         vp]
+        L.zoomr_append_track.argtypes = [vp, i32, vp, vp, i32, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, i32, vp, vp,
+                                         vp, vp, vp]
         L.zoomr_append_track.restype = C.c_int
         L.zoomr_shard_index.argtypes = [i32, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp]
         L.zoomr_shard_index.restype = C.c_int
@@ -495,13 +495,18 @@ def write_newest_kv(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, seq_
 
 
 def append_track(shape: Shape, k_pool, v_pool, page_table, k_new, v_new, token_ids, begin_id, end_id, boundary_ids,
-                 seq_len, bounds, num_summaries, state, close_items, update, dev_status=None, stream=None):
-    """zoomr_append_track: append_kv + track_segments in one launch (PDL behind a chained a5).
-    The pools may be pinned host tensors (the host tier)."""
+                 seq_len, bounds, num_summaries, state, close_items, update, dev_status=None, stream=None,
+                 mirror=None, mirror_page_size=0):
+    """zoomr_append_track: append_kv + track_segments without a host round trip (PDL
+    behind a chained a5).  The pools may be pinned host tensors (the host tier);
+    mirror = (k, v, page_table) of a second pool (page size mirror_page_size) that
+    also gets the rows where their page is resident (the tier's HBM hot pool)."""
     g, kv = shape.c(), _kv(k_pool, v_pool, page_table, host_ok=True)
+    mkv = _kv(*mirror) if mirror is not None else None
     nb = 0 if boundary_ids is None else boundary_ids.numel()
     rc = lib().zoomr_append_track(
-        C.byref(g), k_new.shape[0], C.byref(kv), _ptr(k_new, torch.bfloat16, "k_new"), _ptr(v_new, torch.bfloat16, "v_new"),
+        C.byref(g), k_new.shape[0], C.byref(kv), C.byref(mkv) if mkv is not None else None, int(mirror_page_size),
+        _ptr(k_new, torch.bfloat16, "k_new"), _ptr(v_new, torch.bfloat16, "v_new"),
         _ptr(token_ids, torch.int32, "token_ids"), int(begin_id), int(end_id),
         _ptr(boundary_ids, torch.int32, "boundary_ids") if nb else None, nb, _ptr(seq_len, torch.int32, "seq_len"),
         _ptr(bounds, torch.int32, "bounds"), _ptr(num_summaries, torch.int32, "num_summaries"), bounds.shape[1],

@@ -33,7 +33,7 @@ kin = torch.randn(B, cfg.L, cfg.Hkv, cfg.d, device="cuda").bfloat16()
 vin = torch.randn_like(kin)
 toks = torch.tensor([[200 if (i % 35) == 34 else 7] * B for i in range(N_TOK)], dtype=torch.int32, device="cuda")
 host_k, host_v = inp.k_pool.cpu().pin_memory(), inp.v_pool.cpu().pin_memory()
-ph = 16
+ph = int(os.environ.get("PH", "16"))
 variants = {
     "hbm_chained": lambda: DecodeLoop(shape, B, inp.bounds.shape[1], cfg.T, prm, 1000, 1001, [200]),
     "hbm_plain": lambda: DecodeLoop(shape, B, inp.bounds.shape[1], cfg.T, prm, 1000, 1001, [200], chained=False,
@@ -43,6 +43,15 @@ variants = {
                                    hot_page_size=ph),
 }
 only = os.environ.get("ONLY")
+# diagnosis only: SKIP=newest,fetch drops those launches from the tier loop (results then
+# stale in steady state only by the newest row / no residency update)
+skip = set(filter(None, os.environ.get("SKIP", "").split(",")))
+if skip:
+    if "newest" in skip:
+        Z.write_newest_kv = lambda *a, **k: None
+    if "fetch" in skip:
+        import paper_2604_10898_b200.tier as T_
+        T_.Z.tier_fetch = lambda *a, **k: None
 res = {}
 for name, mk in variants.items():
     if only and name not in only.split(","):

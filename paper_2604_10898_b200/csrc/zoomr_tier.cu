@@ -17,6 +17,7 @@
 namespace zoomr {
 
 constexpr int kPlanThreads = 1024;
+constexpr int kPlanSmemNP = 4096;  // hot-page-table entries (B * max_pages * R) kept in shared memory
 
 __device__ __forceinline__ int tier_block_scan(int x, int *wsum, int *total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -60,17 +61,28 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
   __shared__ int hist[256];
   __shared__ unsigned long long s_prefix;
   __shared__ int s_need;
+  extern __shared__ int plan_smem[];  // [NP] need, [NP] hot page table (when NP <= kPlanSmemNP)
   // launched with PDL behind the select: the copy kernel may launch now (it waits
   // for this plan), and I_f / its count are read only after the select completed
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x;
   const int hmp = max_pages * R;
   const int NP = B * hmp;
-  int32_t *need = ws + 2, *missing = need + NP, *fetch_hot = missing + hot_pages, *fetch_host = fetch_hot + hot_pages;
+  int32_t *missing = ws + 2 + NP, *fetch_hot = missing + hot_pages, *fetch_host = fetch_hot + hot_pages;
+  // The page marks and a snapshot of the hot page table live in shared memory when
+  // they fit; both are set up before the wait (the select writes neither, and the
+  // previous step's plan / copy have completed), so after the wait the plan costs
+  // the I_f load and nothing else until the block scan.
+  const bool in_smem = NP <= kPlanSmemNP;
+  int32_t *need = in_smem ? plan_smem : ws + 2;
+  const int32_t *hpt = in_smem ? plan_smem + NP : hot_pt;
+  for (int x = tid; x < NP; x += kPlanThreads) {
+    need[x] = 0;
+    if (in_smem) plan_smem[NP + x] = hot_pt[x];
+  }
   const int step = ws[0] + 1;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // 1. pages touched by I_f
-  for (int x = tid; x < NP; x += kPlanThreads) need[x] = 0;
   __syncthreads();
   for (int b = 0; b < B; ++b) {
     int n = count[b];
@@ -96,7 +108,7 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
     const int x = x0 + tid;
     bool miss = false;
     if (x < NP && need[x]) {
-      const int h = hot_pt[x];
+      const int h = hpt[x];
       if (h >= 0 && h < hot_pages) stamp[h] = step;
       else miss = true;
     }
@@ -362,7 +374,8 @@ extern "C" int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoo
   const int64_t row = (int64_t)Ph * geom->head_dim * 2;  // bytes of one (page, layer, head) block of the hot pool
   if (row % 16) return ZOOMR_ERR_UNSUPPORTED;
   cudaStream_t s = (cudaStream_t)stream;
-  launch_pdl(tier_plan_kernel, 1, kPlanThreads, 0, s, batch, index, index_count, index_capacity, Ph, R,
+  const size_t plan_smem = batch * hmp <= kPlanSmemNP ? (size_t)2 * batch * hmp * sizeof(int32_t) : 0;
+  launch_pdl(tier_plan_kernel, 1, kPlanThreads, plan_smem, s, batch, index, index_count, index_capacity, Ph, R,
              host_kv->max_pages, host_kv->page_table, hot_page_table, hot_owner, hot_stamp, hot_pages,
              (int32_t *)workspace, dev_status, seq_len);
   rc = launch_status(s);

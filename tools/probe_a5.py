@@ -27,7 +27,8 @@ prm = StepParams(cfg.top_k, cfg.c, cfg.sink, cfg.window)
 sets = []
 for r in range(R):
     inp = S.generate(cfg, device="cuda", seed=cfg.seed + 17 * r)
-    st = ZoomrStep(shape, inp.q.shape[0], inp.bounds.shape[1], cfg.T, prm)
+    st = ZoomrStep(shape, inp.q.shape[0], inp.bounds.shape[1], cfg.T, prm,
+                   early_known=os.environ.get("EARLY", "1") == "1")
     kv = (inp.k_pool, inp.v_pool, inp.page_table)
     seg = (inp.bounds, inp.num_summaries, inp.seq_len)
     st.update_mean_keys(kv, seg, st.all_items(inp.num_summaries))

@@ -107,8 +107,12 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   // run from a warm instruction cache instead of fetching each new block of code
   // through an L2 that a5's gather keeps flushing), then waits for their count
   const bool tail_cta = p.designated_tail && lg == nlg;
+  // a selection update for b this step (else a2 / a3 are skipped and the flags held)
+  const bool upd = !p.update || p.update[b];
 #ifndef ZOOMR_AB_NO_WARM  // A/B builds only: the tail CTA without the warm-up pass
-  if (tail_cta) {
+  // (only when a3 will run: without an update the tail is collect + a4, and the
+  // warm-up pass would sit on its critical path)
+  if (tail_cta && upd) {
     SmemCarve sm{smem_raw};
     long long *A = sm.take<long long>(MS);
     int *v = sm.take<int>(MS);
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   constexpr int kQPT = (G * D + 255) / 256;  // per thread (256 threads)
   float qreg[kQPT];
   const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
-  if (!tail_only && !tail_cta) {
+  if (upd && !tail_only && !tail_cta) {
 #pragma unroll
     for (int j = 0; j < kQPT; ++j) {
       const int x = threadIdx.x + j * 256;
@@ -171,7 +175,6 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   }
 
   // ---- a2: alpha + per-voter top-k (only at a selection update) ---------------------
-  const bool upd = !p.update || p.update[b];
   if (upd && !tail_only && !tail_cta) {
     float *qs = reinterpret_cast<float *>(smem_raw);                 // [G][D]
     float *al = qs + G * D;                                          // [G][MS]

@@ -109,6 +109,17 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
   const bool tail_cta = p.designated_tail && lg == nlg;
   // a selection update for b this step (else a2 / a3 are skipped and the flags held)
   const bool upd = !p.update || p.update[b];
+  // Nothing for the (l, g) CTAs of b to do (no update, no summary closing: a decode
+  // loop's typical token): they exit without counting and the tail CTA goes
+  // straight to a4 instead of waiting for their arrivals.  Every CTA of b
+  // evaluates the same condition from the same inputs.
+  bool idle = false;
+  if (p.designated_tail && p.mode == kFull && !upd) {
+    idle = true;
+    for (int it = 0; it < p.n_items; ++it)
+      if (p.items[2 * it] == b && p.items[2 * it + 1] >= 0) idle = false;
+  }
+  if (idle && !tail_cta) return;
 #ifndef ZOOMR_AB_NO_WARM  // A/B builds only: the tail CTA without the warm-up pass
   // (only when a3 will run: without an update the tail is collect + a4, and the
   // warm-up pass would sit on its critical path)
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.ws_ticket + b) : "memory");
     return;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !idle) {
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ws_ticket + b) : "memory");

@@ -519,8 +519,10 @@ size_t zoomr_tier_workspace_bytes(int32_t batch, int32_t hot_max_pages, int32_t 
  * position seq_len[b] -- the NEXT token's -- resident now (look-ahead), so that
  * at the next step every sink and window page is resident before that step's
  * plan runs (its a5 may then read their entries early, see
- * zoomr_sparse_decode_attn_lse, and zoomr_write_newest_kv finds the newest
- * token's page resident before the selection). */
+ * zoomr_sparse_decode_attn_lse, and zoomr_append_track's mirror /
+ * zoomr_write_newest_kv find the newest token's page resident).  When
+ * seq_len[b] is a multiple of hot_page_size the page holds no row yet: it is
+ * allocated without copying anything from the host. */
 int zoomr_tier_fetch(const zoomr_geom *geom, int32_t batch, const zoomr_kv *host_kv, void *hot_k, void *hot_v,
                      int32_t hot_pages, int32_t hot_page_size, int32_t *hot_page_table, int32_t *hot_owner,
                      int32_t *hot_stamp, const int32_t *index, const int32_t *index_count,

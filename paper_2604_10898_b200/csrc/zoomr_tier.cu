@@ -93,14 +93,22 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
       if (t < 0 || lp >= hmp) set_status(status, ZOOMR_ERR_INDEX_RANGE);
       else need[b * hmp + lp] = 1;
     }
-    // look-ahead: the page of position T (the next token's) is made resident now, so
-    // that in the next step every sink / window page is resident before that step's
-    // plan runs -- its a5 may then read their page entries before its wait
-    if (seq_len && tid == 0) {
-      const int lp = seq_len[b] / Ph;
-      if (seq_len[b] >= 0 && lp < hmp) need[b * hmp + lp] = 1;
-    }
   }
+  __syncthreads();
+  // look-ahead: the page of position T (the next token's) is made resident now, so
+  // that in the next step every sink / window page is resident before that step's
+  // plan runs -- its a5 may then read their page entries before its wait.  When T
+  // starts the page, none of its rows exists yet: it is allocated without a copy
+  // (mark 2; the appends write its rows one by one) -- else it would be a page of
+  // rows from the host copied every Ph tokens for nothing
+  if (seq_len)
+    for (int b = tid; b < B; b += kPlanThreads) {
+      const int T = seq_len[b], lp = T / Ph;
+      if (T >= 0 && lp < hmp) {
+        if (T % Ph == 0) atomicCAS(&need[b * hmp + lp], 0, 2);
+        else need[b * hmp + lp] = 1;
+      }
+    }
   __syncthreads();
   // 2. resident ones are stamped with this step; the others are missing (in page order)
   int nmiss = 0;
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kPlanThreads) tier_plan_kernel(
       const int xb = x / hmp, lph = x - xb * hmp;
       const int hp = host_pt[xb * max_pages + lph / R];
       fetch_hot[j] = h;
-      fetch_host[j] = hp < 0 ? -1 : hp * R + lph % R;
+      fetch_host[j] = hp < 0 ? -1 : need[x] == 2 ? -2 : hp * R + lph % R;  // -2: allocate only (no copy)
       if (hp < 0) set_status(status, ZOOMR_ERR_INDEX_RANGE);
     }
     nv += tot;

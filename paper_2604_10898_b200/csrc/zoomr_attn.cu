@@ -570,8 +570,15 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
       // the last len % 8 rows of a run of >= 8: one more 8-row box ending at the run's
       // end, overlapping the previous box (the overlapped rows are written twice with
       // the same bytes); only runs shorter than 8 rows go through cp.async
+#ifdef ZOOMR_AB_TAILBOX  // A/B builds only: one more 8-row box ending at the run's end, overlapping the
+      // previous box, instead of len % 8 rows by cp.async (index-only a5 -0.6 us at 8B-16K, but the step
+      // +0.5 us there and +8..23 us at configs[4] L_R = 1024, c = 32: kept out)
       const bool leadT = S::SWZ && !whole && cok && len >= 8 && (len & 7) && pos == len - 8;
       const bool byhand = !cok || !S::SWZ || (len < 8 && pos >= n16 + n8);
+#else
+      const bool leadT = false;
+      const bool byhand = !cok || !S::SWZ || pos >= n16 + n8;
+#endif
       const unsigned m16 = __ballot_sync(0xffffffffu, lead16), m8 = __ballot_sync(0xffffffffu, lead8 || leadT);
       const uint32_t tx = (uint32_t)((__ballot_sync(0xffffffffu, lead32) ? 32 : 0) * S::RB * 2 +
                                      (__popc(m16) * 16 + __popc(m8) * 8) * S::RB * 2);

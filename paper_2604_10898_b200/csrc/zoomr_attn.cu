@@ -646,6 +646,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
         }
       }
       cp_async_arrive_noinc(&fullp[s]);
+#ifdef ZOOMR_AB_PROD_DELAY  // A/B builds only: does the producer pace the stream? (it does not)
+      __nanosleep(ZOOMR_AB_PROD_DELAY);
+#endif
       if (k == ntiles - 1) {
         TL(6);
         TLW_SET(gw, 6, TL_NOW());
@@ -1038,6 +1041,9 @@ __global__ void __launch_bounds__(64 * kPairs, 1)
     const int nvalid = min(kTile, cnt - tis * kTile);
     const int s = (int)(k % kStages);
     mbar_wait(&fullp[s], (uint32_t)((k / kStages) & 1), 5000000 + (int)k);
+#ifdef ZOOMR_AB_CONS_DELAY  // A/B builds only: does the math warp pace the stream? (it does not)
+    __nanosleep(ZOOMR_AB_CONS_DELAY);
+#endif
     if (k == 0) {
       TL(3);
 #ifdef ZOOMR_TL_RAMP

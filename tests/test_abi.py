@@ -62,3 +62,33 @@ def test_host_argument_errors_without_a_device(lib):
     lib.zoomr_attn_workspace_bytes.restype = C.c_size_t
     assert lib.zoomr_attn_workspace_bytes(C.byref(bad), 1) == 0
     assert lib.zoomr_build_index(1, None, None, 4, 0, None, 16, None, None, None) == 1
+
+
+def test_round2_entry_points_reject_bad_arguments_without_a_device(lib):
+    """The entry points added in round 2 validate on the host: NULL or inconsistent
+    arguments return ZOOMR_ERR_INVALID_ARG (1) before anything is enqueued."""
+    from paper_2604_10898_b200 import zoomr as Z
+    g = Z.Geom(32, 32, 8, 128, 64)
+    i32 = C.c_int32
+    # zoomr_append_track: no pools / no outputs
+    assert lib.zoomr_append_track(C.byref(g), 1, None, None, 0, None, None, None, 0, 0, None, 0, None, None, None, 8,
+                                  None, None, None, None, None) == 1
+    kv = Z.KV(C.c_void_p(256), C.c_void_p(256), 4, C.c_void_p(256), 4)
+    dummy = C.c_void_p(256)
+    # a mirror pool without a page size
+    mirror = Z.KV(C.c_void_p(256), C.c_void_p(256), 4, C.c_void_p(256), 4)
+    assert lib.zoomr_append_track(C.byref(g), 1, C.byref(kv), C.byref(mirror), 0, dummy, dummy, dummy, 0, 1, None,
+                                  0, dummy, dummy, dummy, 8, dummy, dummy, dummy, None, None) == 1
+    # negative boundary count
+    assert lib.zoomr_append_track(C.byref(g), 1, C.byref(kv), None, 0, dummy, dummy, dummy, 0, 1, None, -1, dummy,
+                                  dummy, dummy, 8, dummy, dummy, dummy, None, None) == 1
+    # zoomr_sparse_decode_attn_lse_chained needs the lse output
+    assert lib.zoomr_sparse_decode_attn_lse_chained(
+        C.byref(g), 1, dummy, C.byref(kv), dummy, None, dummy, 64, None, 0, 0, C.c_float(0.1), 0, 0, dummy, None,
+        dummy, C.c_size_t(1 << 20), None, None) == 1
+    # zoomr_select_front / zoomr_select_tail / zoomr_tier_gather_slice: NULL inputs
+    assert lib.zoomr_select_front(C.byref(g), 1, None, None, None, None, 0, None, None, 2, None, None, None, None,
+                                  C.c_size_t(0), None, None) == 1
+    assert lib.zoomr_select_tail(C.byref(g), 1, None, None, None, None, 2, 4, 8, None, None, None, None, 16, None,
+                                 None, None) == 1
+    assert lib.zoomr_tier_gather_slice(C.byref(g), 1, None, None, None, 16, 0, 1, None, None, 64, 4, None, None) == 1

@@ -43,15 +43,12 @@ variants = {
                                    hot_page_size=ph),
 }
 only = os.environ.get("ONLY")
-# diagnosis only: SKIP=newest,fetch drops those launches from the tier loop (results then
-# stale in steady state only by the newest row / no residency update)
+# diagnosis only: SKIP=fetch drops the tier fetch from the loop (valid only once every page
+# the replayed tokens touch is resident, i.e. from the second pass of the graph on)
 skip = set(filter(None, os.environ.get("SKIP", "").split(",")))
-if skip:
-    if "newest" in skip:
-        Z.write_newest_kv = lambda *a, **k: None
-    if "fetch" in skip:
-        import paper_2604_10898_b200.tier as T_
-        T_.Z.tier_fetch = lambda *a, **k: None
+if "fetch" in skip:
+    import paper_2604_10898_b200.tier as T_
+    T_.Z.tier_fetch = lambda *a, **k: None
 res = {}
 for name, mk in variants.items():
     if only and name not in only.split(","):

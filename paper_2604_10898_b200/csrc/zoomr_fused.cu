@@ -81,8 +81,12 @@ struct FusedParams {
 // the five separate ones, and a5's early rows still overlap the tail.
 enum FusedMode : int { kFull = 0, kFront = 1, kTail = 2 };
 
-template <int D, int G>
-__global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams p) {
+// kT threads per CTA: 256 (two CTAs per SM) when the grid fits in about one wave;
+// 128 (four per SM) for large batches, where the (l, g, b) CTAs come in many
+// waves and each one's front end is a chain of dependent round trips -- twice
+// the CTAs in flight hide twice the latency (configs[2]: 64 x 257 CTAs).
+template <int D, int G, int kT = 256>
+__global__ void __launch_bounds__(kT, 512 / kT) fused_select_kernel(const FusedParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int ticket_last;
   if (!p.pdl_front) allow_dependents();  // a5 may launch and run its prologue; it waits for our completion
@@ -152,13 +156,13 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
 #endif
   // the G queries of this (l, g): loaded now, so that the load overlaps a1's chain
   // instead of adding a round trip between a1 and the scoring
-  constexpr int kQPT = (G * D + 255) / 256;  // per thread (256 threads)
+  constexpr int kQPT = (G * D + kT - 1) / kT;  // per thread
   float qreg[kQPT];
   const __nv_bfloat16 *qb = p.q + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * D;
   if (upd && !tail_only && !tail_cta) {
 #pragma unroll
     for (int j = 0; j < kQPT; ++j) {
-      const int x = threadIdx.x + j * 256;
+      const int x = threadIdx.x + j * kT;
       qreg[j] = x < G * D ? __bfloat162float(qb[x]) : 0.f;
     }
   }
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
     float *ao = p.alpha_out ? p.alpha_out + (((int64_t)b * p.L + l) * Hq + (int64_t)g * G) * MS : nullptr;
 #pragma unroll
     for (int j = 0; j < kQPT; ++j) {
-      const int x = threadIdx.x + j * 256;
+      const int x = threadIdx.x + j * kT;
       if (x < G * D) qs[x] = qreg[j];
     }
     __syncthreads();
@@ -346,8 +350,8 @@ __global__ void __launch_bounds__(256, 2) fused_select_kernel(const FusedParams 
 }
 
 template <int D, int G>
-size_t fused_smem_bytes(int MS, int top_k, int max_pages) {
-  const size_t a1 = 8 * (256 / 32) * D;
+size_t fused_smem_bytes(int MS, int top_k, int max_pages, int threads = 256) {
+  const size_t a1 = 8 * (size_t)(threads / 32) * D;
   const size_t a2 = (size_t)G * D * 4 + (size_t)G * MS * 4 + (size_t)G * top_k * 8;
   const size_t a3 = (size_t)MS * (8 + 4 + 8 + 16 + 1) + (kHistBins + 40) * 4 + (size_t)max_pages * 4 + 9 * 16;
   return a1 > a2 ? (a1 > a3 ? a1 : a3) : (a2 > a3 ? a2 : a3);
@@ -446,15 +450,18 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   const int G = geom->num_q_heads / geom->num_kv_heads;
   dim3 grid(mode == kTail ? 1 : geom->num_layers * geom->num_kv_heads, batch);
   const int max_pages = p.max_pages;
+  /* more than one wave of 256-thread CTAs (two per SM): 128-thread CTAs, four per SM */
+  const bool many = mode != kTail && (int64_t)(grid.x + 1) * grid.y > (int64_t)2 * num_sms();
+  const int nthr = many ? 128 : 256;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
-    auto kfn = fused_select_kernel<DD, GG>;                                                      \
-    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, max_pages);         \
+    auto kfn = many ? fused_select_kernel<DD, GG, 128> : fused_select_kernel<DD, GG, 256>;      \
+    const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, max_pages, nthr);   \
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     prefer_max_smem(kfn);                                                                        \
     int per_sm = 0;                                                                              \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem);                      \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, smem);                     \
     /* the designated tail CTA spins until the (l, g) CTAs of its sequence have counted;    \
        those never wait on anything, so they progress whenever any slot is free -- the B    \
        tail CTAs never fill the GPU, since the whole grid fits at once (checked here).  The \
@@ -464,9 +471,9 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
     p.designated_tail = kDesignatedTail && mode != kTail &&                                      \
                         (int64_t)(grid.x + 1) * grid.y <= (int64_t)per_sm * num_sms();           \
     if (p.designated_tail) grid.x += 1; /* + the tail CTA of each sequence */                   \
-    if (p.pdl_front) launch_pdl(kfn, grid, 256, smem, s, p);                                     \
-    else if (p.designated_tail) launch_cooperative(kfn, grid, 256, smem, s, p);                  \
-    else kfn<<<grid, 256, smem, s>>>(p);                                                         \
+    if (p.pdl_front) launch_pdl(kfn, grid, nthr, smem, s, p);                                    \
+    else if (p.designated_tail) launch_cooperative(kfn, grid, nthr, smem, s, p);                 \
+    else kfn<<<grid, nthr, smem, s>>>(p);                                                        \
   } while (0)
 #define ZOOMR_FS_G(DD)               \
   switch (G) {                       \

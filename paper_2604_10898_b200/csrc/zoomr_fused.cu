@@ -82,9 +82,9 @@ struct FusedParams {
 enum FusedMode : int { kFull = 0, kFront = 1, kTail = 2 };
 
 // kT threads per CTA: 256 (two CTAs per SM) when the grid fits in about one wave;
-// 128 (four per SM) for large batches, where the (l, g, b) CTAs come in many
-// waves and each one's front end is a chain of dependent round trips -- twice
-// the CTAs in flight hide twice the latency (configs[2]: 64 x 257 CTAs).
+// 64 (eight per SM) for large batches, where the (l, g, b) CTAs come in many
+// waves and each one's front end is a chain of dependent round trips -- four
+// times the CTAs in flight hide that latency (configs[2]: 64 x 257 CTAs).
 template <int D, int G, int kT = 256>
 __global__ void __launch_bounds__(kT, 512 / kT) fused_select_kernel(const FusedParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -450,12 +450,15 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   const int G = geom->num_q_heads / geom->num_kv_heads;
   dim3 grid(mode == kTail ? 1 : geom->num_layers * geom->num_kv_heads, batch);
   const int max_pages = p.max_pages;
-  /* more than one wave of 256-thread CTAs (two per SM): 128-thread CTAs, four per SM */
+  /* more than one wave of 256-thread CTAs (two per SM): 64-thread CTAs, eight per SM */
   const bool many = mode != kTail && (int64_t)(grid.x + 1) * grid.y > (int64_t)2 * num_sms();
-  const int nthr = many ? 128 : 256;
+#ifndef ZOOMR_MANY_THREADS  // (A/B builds: 128 or 32)
+#define ZOOMR_MANY_THREADS 64
+#endif
+  const int nthr = many ? ZOOMR_MANY_THREADS : 256;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
-    auto kfn = many ? fused_select_kernel<DD, GG, 128> : fused_select_kernel<DD, GG, 256>;      \
+    auto kfn = many ? fused_select_kernel<DD, GG, ZOOMR_MANY_THREADS> : fused_select_kernel<DD, GG, 256>; \
     const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, max_pages, nthr);   \
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \

@@ -147,3 +147,16 @@ def test_qwen_shape_g7_full_size_sampled():
     rep = {}
     PY.check_sequence_sampled(inp, st, 0, rep)  # every (layer, head)
     print(rep)
+
+
+def test_many_wave_select_grids_qwen_batch3():
+    """A grid of more than one wave of 256-thread CTAs takes the select's small-CTA
+    instantiation (64 threads, eight per SM): G = 7 at batch 3 (3 x 113 CTAs) -- a1
+    bit-exact, votes exact, flags / I_f exact, sampled attention within the rule."""
+    cfg = dataclasses.replace(S.CONFIGS["qwen7b16k"], batch=3, seed=77)
+    inp = S.generate(cfg, device="cuda")
+    st = _run(inp, capacity=8192)
+    rep = {}
+    for b in range(3):
+        PY.check_sequence_sampled(inp, st, b, rep, layers=[0, 27], qheads=[0, 13, 27])
+    print(rep)

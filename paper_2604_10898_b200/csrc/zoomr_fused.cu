@@ -455,10 +455,14 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
 #ifndef ZOOMR_MANY_THREADS  // (A/B builds: 128 or 32)
 #define ZOOMR_MANY_THREADS 64
 #endif
-  const int nthr = many ? ZOOMR_MANY_THREADS : 256;
+  /* a grid of at most one CTA per SM (e.g. one KV head's 80 layers): 512-thread CTAs */
+  const bool few = mode != kTail && (int64_t)(grid.x + 1) * grid.y <= (int64_t)num_sms();
+  const int nthr = many ? ZOOMR_MANY_THREADS : few ? 512 : 256;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \
-    auto kfn = many ? fused_select_kernel<DD, GG, ZOOMR_MANY_THREADS> : fused_select_kernel<DD, GG, 256>; \
+    auto kfn = many  ? fused_select_kernel<DD, GG, ZOOMR_MANY_THREADS>                           \
+               : few ? fused_select_kernel<DD, GG, 512>                                          \
+                     : fused_select_kernel<DD, GG, 256>;                                         \
     const size_t smem = fused_smem_bytes<DD, GG>(seg->max_summaries, top_k, max_pages, nthr);   \
     if (smem > 200 * 1024) return ZOOMR_ERR_UNSUPPORTED;                                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \

@@ -456,7 +456,11 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
 #define ZOOMR_MANY_THREADS 64
 #endif
   /* a grid of at most one CTA per SM (e.g. one KV head's 80 layers): 512-thread CTAs */
-  const bool few = mode != kTail && (int64_t)(grid.x + 1) * grid.y <= (int64_t)num_sms();
+#ifndef ZOOMR_FEW_MODES
+#define ZOOMR_FEW_MODES 1  // 1: kFull only; 2: kFull and kFront
+#endif
+  const bool few = (mode == kFull || (ZOOMR_FEW_MODES == 2 && mode == kFront)) &&
+                   (int64_t)(grid.x + 1) * grid.y <= (int64_t)num_sms();
   const int nthr = many ? ZOOMR_MANY_THREADS : few ? 512 : 256;
 #define ZOOMR_FS(DD, GG)                                                                         \
   do {                                                                                           \

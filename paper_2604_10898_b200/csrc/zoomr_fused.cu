@@ -451,7 +451,7 @@ static int select_fused(const zoomr_geom *geom, int32_t batch, const void *q, co
   dim3 grid(mode == kTail ? 1 : geom->num_layers * geom->num_kv_heads, batch);
   const int max_pages = p.max_pages;
   /* more than one wave of 256-thread CTAs (two per SM): 64-thread CTAs, eight per SM */
-  const bool many = mode != kTail && (int64_t)(grid.x + 1) * grid.y > (int64_t)2 * num_sms();
+  const bool many = mode == kFull && (int64_t)(grid.x + 1) * grid.y > (int64_t)2 * num_sms();
 #ifndef ZOOMR_MANY_THREADS  // (A/B builds: 128 or 32)
 #define ZOOMR_MANY_THREADS 64
 #endif
